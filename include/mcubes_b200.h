@@ -1,0 +1,204 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * mcubes_b200 C ABI -- the FFI boundary of the B200 m-Cubes path
+ * (libmcubes_b200.so, built from paper_2202_01753_b200/csrc/).
+ *
+ * The reference is a header-only C++20 template library with no C ABI
+ * (SURVEY.md section 8b); each entry point below is the C-callable form of the
+ * reference function it replaces, cited as path:line under
+ * /root/reference/proj/include/mcubes/.  C++ users can instead include
+ * <mcubes_b200/mcubes.cuh>, the source-compatible template API, and pass their
+ * own device functors.  Python binds this header via ctypes
+ * (paper_2202_01753_b200/_lib.py); see INTEGRATION.md.
+ *
+ * Conventions: plain pointers + sizes, caller-owned HOST buffers (never
+ * retained), row-major dims x n_bins matrices (grid.hpp:303,
+ * accumulators.hpp:26-27).  Every call returns an int status:
+ *   MCB_OK, MCB_EINVAL (std::invalid_argument), MCB_ENONFINITE
+ *   (NonFiniteSample; query mcb_last_nonfinite), MCB_ECUDA, MCB_EINTERNAL.
+ * A context must be used from one host thread at a time; separate contexts
+ * may run concurrently.
+ */
+#ifndef MCUBES_B200_H
+#define MCUBES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCB_ABI_VERSION 1
+#define MCB_XWORDS 67 /* u64 words per exact accumulator in the exchange buffer */
+
+enum mcb_status {
+  MCB_OK = 0,
+  MCB_EINVAL = -1,
+  MCB_ENONFINITE = -2,
+  MCB_ECUDA = -3,
+  MCB_EINTERNAL = -9
+};
+
+/* Built-in integrands (the reference's suite, integrands.hpp:107-215, plus
+ * the stateful table integrand of BASELINE config 4 and the small functors
+ * the reference's unit tests use). */
+enum mcb_integrand_id {
+  MCB_F1 = 1, /* oscillatory        cos(sum (i+1) x_i)                 */
+  MCB_F2 = 2, /* product peak       prod 1/(1/2500 + (x_i-1/2)^2)      */
+  MCB_F3 = 3, /* corner peak        (1 + sum (i+1) x_i)^(-d-1)         */
+  MCB_F4 = 4, /* Gaussian           exp(-625 sum (x_i-1/2)^2)          */
+  MCB_F5 = 5, /* C0                 exp(-10 sum |x_i-1/2|)             */
+  MCB_F6 = 6, /* discontinuous      exp(sum (i+5) x_i) below cutoffs   */
+  MCB_FA = 7, /* sin(sum x) on (0,10)^6                                */
+  MCB_FB = 8, /* normalized 9D Gaussian on (-1,1)^9                    */
+  MCB_TABLE = 9, /* prod_j lerp(T_j, (x_j-lo_j)*inv_h_j); params =
+                    [n, lo[d], inv_h[d], T_0[n] .. T_{d-1}[n]]          */
+  MCB_T_X0 = 32,         /* x[0]                                          */
+  MCB_T_CONST = 33,      /* params[0]                                     */
+  MCB_T_X0SQ_HALF = 34,  /* x[0]*x[0] + 0.5                               */
+  MCB_T_INF_X0POS = 35,  /* x[0] > 0 ? inf : 1                            */
+  MCB_T_INF = 36,        /* inf                                           */
+  MCB_T_ZERO = 37        /* 0                                             */
+};
+
+enum mcb_bin_update { MCB_BIN_ALL_AXES = 0, MCB_BIN_AXIS0_ONLY = 1 }; /* sampler.hpp:51-54 */
+enum mcb_variant { MCB_VARIANT_MCUBES = 0, MCB_VARIANT_MCUBES1D = 1 }; /* driver.hpp:23 */
+enum mcb_rng { MCB_RNG_COMPAT = 0, MCB_RNG_PHILOX = 1 };
+
+typedef struct mcb_ctx mcb_ctx;
+typedef struct mcb_run mcb_run;
+
+typedef struct {
+  int32_t id;             /* mcb_integrand_id */
+  uint32_t n_params;
+  const double* params;   /* host; copied to the device by the call */
+} mcb_integrand;
+
+/* RunConfig (driver.hpp:37-71) + B200 fields. */
+typedef struct {
+  uint32_t dims;
+  uint32_t n_bins;        /* reference default 50 */
+  uint64_t maxcalls;
+  uint32_t itmax;         /* 15 */
+  uint32_t ita;           /* 10 */
+  double tau_rel;         /* 1e-3 */
+  double alpha;           /* 1.5 */
+  double chi2_dof_max;    /* 1.5 */
+  uint64_t seed;
+  int32_t variant;        /* mcb_variant */
+  uint32_t workers;       /* accepted, ignored (results are worker-invariant) */
+  const double* lower;    /* dims */
+  const double* upper;    /* dims */
+  int32_t rng;            /* mcb_rng */
+  int32_t reserved;
+} mcb_config;
+
+/* IntegrationResult (driver.hpp:181-191). */
+typedef struct {
+  double estimate, sigma, chi2_dof;
+  uint32_t iterations_used;
+  int32_t converged;
+  uint64_t total_samples, bin_writes;
+  uint64_t g, m, p, s; /* SetupParams (driver.hpp:74-79) */
+} mcb_result;
+
+/* IterationResult (driver.hpp:126-130). */
+typedef struct {
+  double estimate, variance;
+  uint32_t index;
+  uint32_t pad;
+} mcb_iteration;
+
+/* IterationView (driver.hpp:196-203); grid_edges is dims*n_bins, valid only
+ * during the callback. */
+typedef struct {
+  uint32_t iteration;
+  int32_t adjusting;
+  mcb_iteration result;
+  double running_estimate, running_sigma, running_chi2_dof;
+  const double* grid_edges;
+  uint64_t bin_writes;
+} mcb_iteration_view;
+typedef void (*mcb_observer)(const mcb_iteration_view* view, void* user);
+
+/* ---- context ---- */
+int mcb_ctx_create(int device, mcb_ctx** out);
+int mcb_ctx_destroy(mcb_ctx* ctx);
+/* Run on a caller-owned cudaStream_t (NULL = the context's own stream). */
+int mcb_ctx_set_stream(mcb_ctx* ctx, void* cuda_stream);
+int mcb_ctx_synchronize(mcb_ctx* ctx);
+/* Kernels launched through this context so far. */
+uint64_t mcb_ctx_launches(const mcb_ctx* ctx);
+const char* mcb_last_error(const mcb_ctx* ctx);
+/* Point (dims doubles) and f(x) of the last MCB_ENONFINITE (sampler.hpp:35-36). */
+int mcb_last_nonfinite(const mcb_ctx* ctx, double* x, uint32_t cap, double* fx);
+int mcb_abi_version(void);
+
+/* ---- one iteration: v_sample (sampler.hpp:312-333) ----
+ * edges: dims*n_bins right edges (NULL = uniform grid on [lower, upper]).
+ * contrib: dims*n_bins out (rows >= bin_axes are zero); writes = m*p*bin_axes. */
+int mcb_v_sample(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,
+                 const double* lower, const double* upper, const double* edges, uint64_t m,
+                 uint64_t s, uint64_t p, uint64_t seed, uint64_t iteration, int32_t bin_update,
+                 double* estimate, double* variance, double* contrib, uint64_t* writes);
+
+/* ---- frozen iteration: v_sample_no_adjust (sampler.hpp:339-349) ---- */
+int mcb_v_sample_no_adjust(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,
+                           const double* lower, const double* upper, const double* edges,
+                           uint64_t m, uint64_t s, uint64_t p, uint64_t seed, uint64_t iteration,
+                           double* estimate, double* variance);
+
+/* ---- Philox-stream variant of v_sample (north-star RNG; not bitwise comparable
+ * with the reference, statistically equivalent). ---- */
+int mcb_v_sample_philox(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,
+                        const double* lower, const double* upper, const double* edges, uint64_t m,
+                        uint64_t s, uint64_t p, uint64_t seed, uint64_t iteration,
+                        int32_t bin_update, double* estimate, double* variance, double* contrib,
+                        uint64_t* writes);
+
+/* ---- grid adaptation on the device: Grid::adjusted / adjusted_symmetric
+ * (grid.hpp:104-146, 232-297).  symmetric != 0 reads contrib row 0 only. ---- */
+int mcb_grid_adjust(mcb_ctx* ctx, uint32_t dims, uint32_t n_bins, const double* lower,
+                    const double* upper, const double* edges, const double* contrib, double alpha,
+                    int32_t symmetric, double* out_edges);
+
+/* ---- host utilities (driver.hpp:82-178) ---- */
+int mcb_setup(const mcb_config* cfg, uint64_t* g, uint64_t* m, uint64_t* p, uint64_t* s);
+int mcb_set_batch_size(uint64_t m, uint32_t workers, uint64_t* s);
+int mcb_weighted_estimate(uint32_t n, const double* estimates, const double* variances,
+                          double* estimate, double* sigma, double* chi2_dof);
+int mcb_check_convergence(double estimate, double sigma, double chi2_dof, double tau_rel,
+                          double chi2_dof_max);
+int mcb_grid_uniform(uint32_t dims, uint32_t n_bins, const double* lower, const double* upper,
+                     double* edges);
+
+/* ---- the full loop: integrate (driver.hpp:215-258) ----
+ * history: caller array of history_cap entries (may be NULL).  observer may be
+ * NULL (then the run is enqueued with a single synchronisation at the end). */
+int mcb_integrate(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, mcb_result* result,
+                  mcb_iteration* history, uint32_t history_cap, mcb_observer observer, void* user);
+
+/* ---- stepped run: the multi-GPU hook.  Each rank samples its slice of the
+ * linear work index, the caller all-reduces (sum, uint64) the exchange buffer
+ * across ranks, then every rank finishes the iteration identically. ---- */
+int mcb_run_create(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, mcb_run** out);
+int mcb_run_destroy(mcb_run* run);
+/* Exchange buffer length (u64 words) for iteration it (1-based). */
+uint64_t mcb_run_exchange_words(const mcb_run* run, uint32_t it);
+/* Use a caller-owned DEVICE buffer (>= max exchange words) for the exchange. */
+int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
+void* mcb_run_exchange_ptr(const mcb_run* run);
+/* Total linear work items (= m cubes). */
+uint64_t mcb_run_work_items(const mcb_run* run);
+int mcb_run_sample(mcb_run* run, uint32_t it, uint64_t n0, uint64_t n1);
+int mcb_run_finish(mcb_run* run, uint32_t it);
+int mcb_run_result(mcb_run* run, mcb_result* result, mcb_iteration* history, uint32_t history_cap);
+/* Current grid edges (dims*n_bins) -- synchronises. */
+int mcb_run_grid(mcb_run* run, double* edges);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MCUBES_B200_H */

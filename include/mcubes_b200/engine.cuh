@@ -1,0 +1,355 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host engine: device context, buffers and the launch sequence of one m-Cubes
+// iteration (K1 sample -> K3a exact cross-block sum -> [all-reduce] -> K3b
+// round -> K4 adapt/combine).  Everything here is stream-ordered; a whole
+// integrate() run is enqueued without a host synchronisation (the device
+// `stop` flag turns iterations after convergence into no-ops).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "config.cuh"
+#include "epilogue.cuh"
+#include "exact.cuh"
+#include "integrands.cuh"
+#include "rng.cuh"
+#include "sampler.cuh"
+
+namespace mcubes::gpu {
+
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " at " + file +
+                    ":" + std::to_string(line));
+}
+#define MCB_CUDA(x) ::mcubes::gpu::cuda_check((x), #x, __FILE__, __LINE__)
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  T* ensure(std::size_t n) {
+    if (n > cap_) {
+      release();
+      MCB_CUDA(cudaMalloc(&p_, sizeof(T) * std::max<std::size_t>(n, 1)));
+      cap_ = n;
+    }
+    return p_;
+  }
+  T* get() const { return p_; }
+  std::size_t capacity() const { return cap_; }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    cap_ = 0;
+  }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t cap_ = 0;
+};
+
+/// Sampling shape of one iteration (checked like check_sample_args,
+/// sampler.hpp:285-295).
+struct Shape {
+  std::uint32_t dims = 0, nb = 0;
+  std::uint64_t m = 0, p = 0, g = 0;
+  std::uint64_t A = 0;  ///< 1 + g + ... + g^(d-1) mod m
+  double scale = 0, rcp_g = 0, pp1 = 0, rcp_pp1 = 0;
+};
+
+/// d-th integer root of m, or 0 (sampler.hpp:184-197).
+inline std::uint64_t exact_root(std::uint64_t m, std::uint32_t d) {
+  const auto guess = static_cast<std::uint64_t>(
+      std::llround(std::pow(static_cast<double>(m), 1.0 / static_cast<double>(d))));
+  for (std::uint64_t g = guess > 2 ? guess - 2 : 1; g <= guess + 2; ++g) {
+    std::uint64_t acc = 1;
+    bool overflow = false;
+    for (std::uint32_t i = 0; i < d && !overflow; ++i) {
+      if (acc > m / g) overflow = true;
+      else acc *= g;
+    }
+    if (!overflow && acc == m) return g;
+  }
+  return 0;
+}
+
+inline Shape make_shape(std::uint32_t dims, std::uint32_t nb, std::uint64_t m, std::uint64_t s,
+                        std::uint64_t p) {
+  if (m == 0) throw std::invalid_argument("v_sample: m must be >= 1");
+  if (p < 2) throw std::invalid_argument("v_sample: p must be >= 2");
+  if (s == 0) throw std::invalid_argument("v_sample: batch size must be >= 1");
+  const std::uint64_t g = exact_root(m, dims);
+  if (g == 0) throw std::invalid_argument("v_sample: m must be a perfect d-th power of the cube count");
+  if (dims > static_cast<std::uint32_t>(kMaxDims))
+    throw std::invalid_argument("B200 path: dims must be <= " + std::to_string(kMaxDims));
+  Shape sh;
+  sh.dims = dims;
+  sh.nb = nb;
+  sh.m = m;
+  sh.p = p;
+  sh.g = g;
+  unsigned __int128 A = 0, pw = 1;
+  for (std::uint32_t j = 0; j < dims; ++j) {
+    A += pw;
+    pw *= g;
+  }
+  sh.A = static_cast<std::uint64_t>(A % m);
+  sh.scale = 1.0 / (static_cast<double>(m) * static_cast<double>(p));  // sampler.hpp:293
+  sh.rcp_g = 1.0 / static_cast<double>(g);
+  sh.pp1 = static_cast<double>(p) * static_cast<double>(p - 1);  // sampler.hpp:178
+  sh.rcp_pp1 = 1.0 / sh.pp1;
+  return sh;
+}
+
+/// A device context: one CUDA device, one stream, reusable scratch.
+/// Use from one host thread at a time; separate contexts may run concurrently.
+class Context {
+ public:
+  explicit Context(int device = -1) {
+    if (device < 0) MCB_CUDA(cudaGetDevice(&device));
+    device_ = device;
+    MCB_CUDA(cudaSetDevice(device_));
+    MCB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_));
+    MCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    stream_ = own_stream_;
+    MCB_CUDA(cudaMallocHost(&pinned_, kPinnedBytes));
+  }
+  ~Context() {
+    cudaSetDevice(device_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
+    if (pinned_) cudaFreeHost(pinned_);
+  }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  int device() const { return device_; }
+  int sms() const { return sms_; }
+  cudaStream_t stream() const { return stream_; }
+  /// Run on a caller-owned stream (e.g. torch's current stream) instead.
+  void set_stream(cudaStream_t s) { stream_ = s ? s : own_stream_; }
+  void activate() const { MCB_CUDA(cudaSetDevice(device_)); }
+  void sync() const { MCB_CUDA(cudaStreamSynchronize(stream_)); }
+
+  /// Number of kernels this context enqueued (our own kernels only).
+  std::uint64_t launches = 0;
+
+  DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var, scalars, point;
+  DevBuf<std::uint32_t> partials;
+  DevBuf<unsigned long long> words, err_key;
+  DevBuf<RunState> state;
+  DevBuf<double> table;  ///< parameters of a stateful integrand (owned copy)
+
+  static constexpr std::size_t kPinnedBytes = 1 << 20;
+  unsigned char* pinned() const { return pinned_; }
+
+ private:
+  int device_ = 0;
+  int sms_ = 0;
+  cudaStream_t own_stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  unsigned char* pinned_ = nullptr;
+};
+
+/// Geometry of one K1 launch (results do not depend on it).
+struct Launch {
+  int blocks = 0;
+  std::size_t smem = 0;
+};
+
+template <class F, int D, RngKind R>
+Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes,
+                 std::uint64_t iter_root, std::uint64_t n0, std::uint64_t n1, const int* stop,
+                 unsigned long long* err_key) {
+  auto kern = vsample_kernel<F, D, R>;
+  Launch L;
+  L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
+  int max_smem = 0;
+  MCB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx.device()));
+  if (L.smem > static_cast<std::size_t>(max_smem))
+    throw std::invalid_argument("B200 path: dims*n_bins too large for the shared-memory histogram (" +
+                                std::to_string(L.smem) + " B > " + std::to_string(max_smem) + " B)");
+  MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
+  int occ = 0;
+  MCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSampleThreads, L.smem));
+  occ = std::max(occ, 1);
+  const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
+  const std::uint64_t want = (work + kSampleThreads - 1) / kSampleThreads;
+  L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
+
+  SampleArgs a{};
+  a.edges = ctx.edges.get();
+  a.lower = ctx.lower.get();
+  a.dims = sh.dims;
+  a.nb = sh.nb;
+  a.bin_axes = bin_axes;
+  a.m = sh.m;
+  a.p = sh.p;
+  a.g = sh.g;
+  a.nbd = static_cast<double>(sh.nb);
+  a.gd = static_cast<double>(sh.g);
+  a.rcp_g = sh.rcp_g;
+  a.scale = sh.scale;
+  a.pp1 = sh.pp1;
+  a.rcp_pp1 = sh.rcp_pp1;
+  a.iter_root = iter_root;
+  a.n0 = n0;
+  a.n1 = n1;
+  a.A = sh.A;
+  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kSampleThreads;
+  a.stepT = static_cast<std::uint64_t>((static_cast<unsigned __int128>(T % sh.m) * sh.A) % sh.m);
+  std::uint64_t st = a.stepT;
+  for (int j = 0; j < kMaxDims; ++j) {
+    a.step_digits[j] = j < static_cast<int>(sh.dims) ? st % sh.g : 0;
+    if (j < static_cast<int>(sh.dims)) st /= sh.g;
+  }
+  const int nacc = block_accs(bin_axes, sh.nb);
+  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * nacc);
+  a.err_key = err_key;
+  a.stop = stop;
+  kern<<<L.blocks, kSampleThreads, L.smem, ctx.stream()>>>(a, f);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+  return L;
+}
+
+template <class F, int D, RngKind R>
+void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_root, std::uint64_t t,
+                  std::uint64_t k, double* out_x, double* out_fx) {
+  SampleArgs a{};
+  a.edges = ctx.edges.get();
+  a.lower = ctx.lower.get();
+  a.dims = sh.dims;
+  a.nb = sh.nb;
+  a.m = sh.m;
+  a.p = sh.p;
+  a.g = sh.g;
+  a.nbd = static_cast<double>(sh.nb);
+  a.gd = static_cast<double>(sh.g);
+  a.rcp_g = sh.rcp_g;
+  a.iter_root = iter_root;
+  const std::size_t smem = sizeof(double) * D * (sh.nb + 1);
+  auto kern = sample_point_kernel<F, D, R>;
+  MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<1, 128, smem, ctx.stream()>>>(a, f, t, k, out_x, out_fx);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+/// Compile-time dimension dispatch.  The set of instantiated dimensions can
+/// be narrowed with MCB_DIMS_MAX to trade compile time for coverage.
+#ifndef MCB_DIMS_MAX
+#define MCB_DIMS_MAX 16
+#endif
+
+template <class F, RngKind R>
+Launch dispatch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes, std::uint64_t iter_root,
+                   std::uint64_t n0, std::uint64_t n1, const int* stop, unsigned long long* err_key) {
+  switch (sh.dims) {
+#define MCB_CASE(D) \
+  case D:           \
+    if constexpr (D <= MCB_DIMS_MAX) return launch_k1<F, D, R>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key); \
+    break;
+    MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
+    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16)
+#undef MCB_CASE
+    default:
+      break;
+  }
+  throw std::invalid_argument("B200 path: no kernel compiled for dims=" + std::to_string(sh.dims));
+}
+
+template <class F, RngKind R>
+void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_root, std::uint64_t t,
+                    std::uint64_t k, double* out_x, double* out_fx) {
+  switch (sh.dims) {
+#define MCB_CASE(D) \
+  case D:           \
+    if constexpr (D <= MCB_DIMS_MAX) { launch_point<F, D, R>(ctx, f, sh, iter_root, t, k, out_x, out_fx); return; } \
+    break;
+    MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
+    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16)
+#undef MCB_CASE
+    default:
+      break;
+  }
+  throw std::invalid_argument("B200 path: no kernel compiled for dims=" + std::to_string(sh.dims));
+}
+
+/// K3a: per-block partials -> exchange words (zeroing the scalar slots first).
+inline void launch_reduce(Context& ctx, const Launch& L, std::uint32_t bin_axes, std::uint32_t nb,
+                          unsigned long long* words, const int* stop) {
+  const int nacc = block_accs(bin_axes, nb);
+  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * kScalarAccs * kXWords, ctx.stream()));
+  const int n = nacc * kXWords;
+  reduce_partials_kernel<0><<<(n + 255) / 256, 256, 0, ctx.stream()>>>(ctx.partials.get(), L.blocks, nacc, words, stop);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+/// K3b: exchange words -> estimate, variance, contributions.
+inline void launch_round(Context& ctx, const Shape& sh, std::uint32_t bin_axes, const unsigned long long* words,
+                         double* est, double* var, double* contrib, const int* stop) {
+  RoundArgs r{};
+  r.words = words;
+  r.dims = sh.dims;
+  r.nb = sh.nb;
+  r.bin_axes = bin_axes;
+  r.md2 = static_cast<double>(sh.m) * static_cast<double>(sh.m);
+  r.est = est;
+  r.var = var;
+  r.contrib = contrib;
+  r.stop = stop;
+  const int n = static_cast<int>(sh.dims * sh.nb + 2);
+  round_kernel<0><<<(n + 127) / 128, 128, 0, ctx.stream()>>>(r);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+inline int adjust_threads(std::uint32_t dims, int symmetric) {
+  const int warps = symmetric ? 4 : std::max<int>(1, std::min<int>(static_cast<int>(dims), 16));
+  return 32 * warps;
+}
+
+inline std::size_t adjust_smem(int threads, std::uint32_t nb) {
+  return sizeof(double) * static_cast<std::size_t>(threads / 32) * 3 * nb;
+}
+
+/// Standalone Grid::adjusted on device (edges in ctx.edges, contributions in
+/// ctx.contrib).
+inline void launch_adjust(Context& ctx, const AdjustArgs& a) {
+  const int th = adjust_threads(a.dims, a.symmetric);
+  const std::size_t smem = adjust_smem(th, a.nb);
+  MCB_CUDA(cudaFuncSetAttribute(adjust_grid_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  adjust_grid_kernel<0><<<1, th, smem, ctx.stream()>>>(a);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+inline void launch_epilogue(Context& ctx, const EpilogueArgs& e) {
+  const int th = adjust_threads(e.adj.dims, e.adj.symmetric);
+  const std::size_t smem = adjust_smem(th, e.adj.nb);
+  MCB_CUDA(cudaFuncSetAttribute(epilogue_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  epilogue_kernel<0><<<1, th, smem, ctx.stream()>>>(e);
+  MCB_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+}  // namespace mcubes::gpu

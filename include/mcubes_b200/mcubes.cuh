@@ -1,0 +1,745 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// mcubes_b200: the B200-native drop-in for the reference's header-only
+// m-Cubes API (proj/include/mcubes/*.hpp).  Same names, fields, layouts and
+// error behaviour in namespace `mcubes`:
+//
+//   RunConfig, setup, set_batch_size, weighted_estimate, check_convergence,
+//   integrate(f, cfg, observer) -> IntegrationResult          (driver.hpp)
+//   v_sample, v_sample_no_adjust, SampleOutcome, BinUpdate,
+//   NonFiniteSample                                            (sampler.hpp)
+//   Grid (transform, adjusted, adjusted_symmetric, write/read) (grid.hpp)
+//   BinAccumulator                                             (accumulators.hpp)
+//
+// The integrand is any trivially copyable functor whose
+// `double operator()(std::span<const double>) const` is __host__ __device__
+// (gpu::DeviceIntegrand).  The sampling iteration, its exact reductions, the
+// grid adaptation and the weighted combination all run on the GPU; compile the
+// including translation unit with nvcc -std=c++20 --expt-relaxed-constexpr
+// -fmad=false (the analogue of the reference's -ffp-contract=off) for
+// bitwise parity with the CPU reference on +-*/ integrands.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <iomanip>
+#include <istream>
+#include <limits>
+#include <map>
+#include <memory>
+#include <optional>
+#include <ostream>
+#include <span>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace mcubes {
+
+// =============================================================== accumulators
+/// Per-axis, per-bin totals of (f(x)*J)^2 (accumulators.hpp:18-56).
+class BinAccumulator {
+ public:
+  BinAccumulator(std::uint32_t dims, std::uint32_t n_bins)
+      : dims_(dims), n_bins_(n_bins), values_(std::size_t{dims} * n_bins, 0.0) {
+    if (dims == 0) throw std::invalid_argument("BinAccumulator: dims must be >= 1");
+    if (n_bins == 0) throw std::invalid_argument("BinAccumulator: n_bins must be >= 1");
+  }
+  BinAccumulator(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> values, std::uint64_t writes)
+      : dims_(dims), n_bins_(n_bins), values_(std::move(values)), writes_(writes) {
+    if (values_.size() != std::size_t{dims} * n_bins)
+      throw std::invalid_argument("BinAccumulator: value matrix has wrong shape");
+  }
+  void deposit(std::uint32_t axis, std::uint32_t bin, double v) {
+    values_[std::size_t{axis} * n_bins_ + bin] += v;
+    ++writes_;
+  }
+  [[nodiscard]] double at(std::uint32_t axis, std::uint32_t bin) const {
+    return values_[std::size_t{axis} * n_bins_ + bin];
+  }
+  [[nodiscard]] std::span<const double> axis_row(std::uint32_t axis) const {
+    if (axis >= dims_) throw std::invalid_argument("BinAccumulator: axis out of range");
+    return {values_.data() + std::size_t{axis} * n_bins_, n_bins_};
+  }
+  [[nodiscard]] const std::vector<double>& values() const { return values_; }
+  [[nodiscard]] std::uint32_t dims() const { return dims_; }
+  [[nodiscard]] std::uint32_t n_bins() const { return n_bins_; }
+  [[nodiscard]] std::uint64_t writes() const { return writes_; }
+
+ private:
+  std::uint32_t dims_;
+  std::uint32_t n_bins_;
+  std::vector<double> values_;
+  std::uint64_t writes_ = 0;
+};
+
+/// Thrown when f(x)*jacobian is not finite; carries the offending point
+/// (sampler.hpp:31-48).  The GPU reports the first failure in serial
+/// (cube, sample) order -- what the serial oracle would throw.
+class NonFiniteSample : public std::runtime_error {
+ public:
+  NonFiniteSample(std::vector<double> x, double fx)
+      : std::runtime_error(describe(x, fx)), point_(std::move(x)), value_(fx) {}
+  [[nodiscard]] const std::vector<double>& point() const { return point_; }
+  [[nodiscard]] double value() const { return value_; }
+
+ private:
+  static std::string describe(const std::vector<double>& x, double fx) {
+    std::ostringstream os;
+    os << "integrand produced non-finite value " << fx << " at x = (";
+    for (std::size_t j = 0; j < x.size(); ++j) os << (j ? ", " : "") << x[j];
+    os << ")";
+    return os.str();
+  }
+  std::vector<double> point_;
+  double value_;
+};
+
+enum class BinUpdate : std::uint8_t { all_axes, axis0_only };
+
+struct SampleOutcome {
+  double raw_estimate;
+  double raw_variance;
+  BinAccumulator contributions;
+};
+
+struct EstimateVariance {
+  double raw_estimate;
+  double raw_variance;
+};
+
+namespace gpu {
+
+/// One context per (host thread, device), created on first use.
+inline Context& default_context() {
+  int dev = 0;
+  MCB_CUDA(cudaGetDevice(&dev));
+  thread_local std::map<int, std::unique_ptr<Context>> ctxs;
+  auto& c = ctxs[dev];
+  if (!c) c = std::make_unique<Context>(dev);
+  return *c;
+}
+
+/// Type-erased launchers of one integrand: lets the (non-template)
+/// orchestration below serve every functor type.
+struct IntegrandOps {
+  std::function<Launch(Context&, const Shape&, std::uint32_t, std::uint64_t, std::uint64_t, std::uint64_t,
+                       const int*, unsigned long long*)>
+      k1;
+  std::function<void(Context&, const Shape&, std::uint64_t, std::uint64_t, std::uint64_t, double*, double*)> point;
+  RngKind rng = RngKind::compat;
+};
+
+template <DeviceIntegrand F, RngKind R = RngKind::compat>
+IntegrandOps make_ops(const F& f) {
+  IntegrandOps ops;
+  ops.k1 = [f](Context& c, const Shape& sh, std::uint32_t ba, std::uint64_t root, std::uint64_t n0,
+               std::uint64_t n1, const int* stop, unsigned long long* err) {
+    return dispatch_k1<F, R>(c, f, sh, ba, root, n0, n1, stop, err);
+  };
+  ops.point = [f](Context& c, const Shape& sh, std::uint64_t root, std::uint64_t t, std::uint64_t k, double* x,
+                  double* fx) { dispatch_point<F, R>(c, f, sh, root, t, k, x, fx); };
+  ops.rng = R;
+  return ops;
+}
+
+/// Per-iteration key: the reference's iteration root (rng.hpp:47-50); the
+/// Philox stream uses the same 64-bit value as its key.
+inline std::uint64_t iteration_key(std::uint64_t seed, std::uint64_t it) { return rng::iteration_root(seed, it); }
+
+inline void upload(Context& ctx, DevBuf<double>& buf, const double* host, std::size_t n) {
+  MCB_CUDA(cudaMemcpyAsync(buf.ensure(n), host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream()));
+}
+
+inline void download(Context& ctx, double* host, const double* dev, std::size_t n) {
+  MCB_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream()));
+}
+
+[[noreturn]] inline void throw_nonfinite(Context& ctx, const IntegrandOps& ops, const Shape& sh,
+                                         std::uint64_t iter_root, unsigned long long key) {
+  double* dx = ctx.point.ensure(sh.dims + 1);
+  ops.point(ctx, sh, iter_root, key / sh.p, key % sh.p, dx, dx + sh.dims);
+  std::vector<double> hx(sh.dims + 1);
+  download(ctx, hx.data(), dx, sh.dims + 1);
+  ctx.sync();
+  const double fx = hx[sh.dims];
+  hx.resize(sh.dims);
+  throw NonFiniteSample(std::move(hx), fx);
+}
+
+}  // namespace gpu
+
+// ====================================================================== grid
+/// Per-axis importance grid (grid.hpp:19-176): right edges only, d x n_bins
+/// row-major, implicit left edge at `lower`.
+class Grid {
+ public:
+  Grid(std::uint32_t dims, std::uint32_t n_bins, std::span<const double> lower, std::span<const double> upper)
+      : dims_(dims), n_bins_(n_bins), lower_(lower.begin(), lower.end()), upper_(upper.begin(), upper.end()),
+        edges_(std::size_t{dims} * n_bins) {
+    if (dims_ == 0) throw std::invalid_argument("Grid: dims must be >= 1");
+    if (n_bins_ < 2) throw std::invalid_argument("Grid: n_bins must be >= 2");
+    if (lower_.size() != dims_ || upper_.size() != dims_)
+      throw std::invalid_argument("Grid: bounds must have one entry per axis");
+    for (std::uint32_t j = 0; j < dims_; ++j) {
+      if (!(lower_[j] < upper_[j]) || !std::isfinite(lower_[j]) || !std::isfinite(upper_[j]))
+        throw std::invalid_argument("Grid: requires finite lower < upper on every axis");
+      double* row = edges_.data() + std::size_t{j} * n_bins_;
+      const double width = (upper_[j] - lower_[j]) / static_cast<double>(n_bins_);
+      for (std::uint32_t i = 0; i + 1 < n_bins_; ++i) row[i] = lower_[j] + static_cast<double>(i + 1) * width;
+      row[n_bins_ - 1] = upper_[j];
+    }
+  }
+
+  /// From raw edges (validated like Grid::read, grid.hpp:530-548).
+  static Grid from_edges(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> lower,
+                         std::vector<double> upper, std::vector<double> edges) {
+    if (dims == 0 || n_bins < 2) throw std::invalid_argument("Grid::read: malformed header");
+    if (lower.size() != dims || upper.size() != dims || edges.size() != std::size_t{dims} * n_bins)
+      throw std::invalid_argument("Grid: bounds must have one entry per axis");
+    return Grid(dims, n_bins, std::move(lower), std::move(upper), std::move(edges));
+  }
+
+  [[nodiscard]] std::uint32_t dims() const { return dims_; }
+  [[nodiscard]] std::uint32_t n_bins() const { return n_bins_; }
+  [[nodiscard]] double lower(std::uint32_t axis) const { return lower_[axis]; }
+  [[nodiscard]] double upper(std::uint32_t axis) const { return upper_[axis]; }
+  [[nodiscard]] std::span<const double> edges(std::uint32_t axis) const {
+    return {edges_.data() + std::size_t{axis} * n_bins_, n_bins_};
+  }
+  [[nodiscard]] const std::vector<double>& raw_edges() const { return edges_; }
+  [[nodiscard]] const std::vector<double>& lowers() const { return lower_; }
+  [[nodiscard]] const std::vector<double>& uppers() const { return upper_; }
+
+  /// grid.hpp:61-67
+  [[nodiscard]] std::uint32_t bin_index(double u) const {
+    const double nb = static_cast<double>(n_bins_);
+    const double z = u * nb;
+    if (!(z > 0.0)) return 0;
+    if (z >= nb) return n_bins_ - 1;
+    return static_cast<std::uint32_t>(z);
+  }
+  void bin_indices(std::span<const double> u, std::span<std::uint32_t> out) const {
+    for (std::uint32_t j = 0; j < dims_; ++j) out[j] = bin_index(u[j]);
+  }
+
+  /// Host form of the map the sampling kernel applies (grid.hpp:204-224).
+  double transform(std::span<const double> u, std::span<double> x) const { return transform_impl<false>(u, x, {}); }
+  double transform(std::span<const double> u, std::span<double> x, std::span<std::uint32_t> bins) const {
+    return transform_impl<true>(u, x, bins);
+  }
+
+  /// One adaptation step (grid.hpp:104-114), computed on the GPU.
+  [[nodiscard]] Grid adjusted(const BinAccumulator& contributions, double alpha) const {
+    if (contributions.dims() != dims_ || contributions.n_bins() != n_bins_)
+      throw std::invalid_argument("Grid::adjusted: contribution shape mismatch");
+    require_valid_alpha(alpha);
+    check_contrib(contributions.values());
+    return adjust_on_device(contributions.values(), alpha, false);
+  }
+
+  /// Symmetric-integrand adaptation (grid.hpp:122-146), computed on the GPU.
+  [[nodiscard]] Grid adjusted_symmetric(std::span<const double> axis0_contributions, double alpha) const {
+    if (axis0_contributions.size() != n_bins_)
+      throw std::invalid_argument("Grid::adjusted_symmetric: contribution shape mismatch");
+    require_valid_alpha(alpha);
+    std::vector<double> c(std::size_t{dims_} * n_bins_, 0.0);
+    std::copy(axis0_contributions.begin(), axis0_contributions.end(), c.begin());
+    check_contrib(c);
+    return adjust_on_device(c, alpha, true);
+  }
+
+  /// Plain-text form (grid.hpp:148-158).
+  void write(std::ostream& os) const {
+    os << dims_ << ' ' << n_bins_ << '\n';
+    const auto saved = os.precision(17);
+    for (std::uint32_t j = 0; j < dims_; ++j) {
+      os << lower_[j] << ' ' << upper_[j];
+      for (const double e : edges(j)) os << ' ' << e;
+      os << '\n';
+    }
+    os.precision(saved);
+  }
+
+  /// grid.hpp:161-174
+  static Grid read(std::istream& is) {
+    std::uint32_t dims = 0, n_bins = 0;
+    if (!(is >> dims >> n_bins) || dims == 0 || n_bins < 2) throw std::invalid_argument("Grid::read: malformed header");
+    std::vector<double> lower(dims), upper(dims), edges(std::size_t{dims} * n_bins);
+    for (std::uint32_t j = 0; j < dims; ++j) {
+      if (!(is >> lower[j] >> upper[j])) throw std::invalid_argument("Grid::read: malformed axis bounds");
+      double* row = edges.data() + std::size_t{j} * n_bins;
+      for (std::uint32_t i = 0; i < n_bins; ++i)
+        if (!(is >> row[i])) throw std::invalid_argument("Grid::read: malformed edge list");
+    }
+    return Grid(dims, n_bins, std::move(lower), std::move(upper), std::move(edges));
+  }
+
+  friend bool operator==(const Grid&, const Grid&) = default;
+
+ private:
+  Grid(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> lower, std::vector<double> upper,
+       std::vector<double> raw_edges)
+      : dims_(dims), n_bins_(n_bins), lower_(std::move(lower)), upper_(std::move(upper)), edges_(std::move(raw_edges)) {
+    for (std::uint32_t j = 0; j < dims_; ++j) {
+      if (!(lower_[j] < upper_[j])) throw std::invalid_argument("Grid: requires lower < upper on every axis");
+      double prev = lower_[j];
+      for (const double e : edges(j)) {
+        if (!(e > prev)) throw std::invalid_argument("Grid: edges must increase strictly");
+        prev = e;
+      }
+      if (edges(j).back() != upper_[j]) throw std::invalid_argument("Grid: last edge must equal the upper bound");
+    }
+  }
+
+  static void require_valid_alpha(double alpha) {
+    if (!(alpha >= 0.0) || !std::isfinite(alpha))
+      throw std::invalid_argument("Grid: damping exponent alpha must be finite and >= 0");
+  }
+  static void check_contrib(const std::vector<double>& c) {
+    for (const double v : c)
+      if (v < 0.0 || !std::isfinite(v)) throw std::invalid_argument("Grid: contributions must be finite and >= 0");
+  }
+
+  Grid adjust_on_device(const std::vector<double>& contrib, double alpha, bool symmetric) const {
+    gpu::Context& ctx = gpu::default_context();
+    ctx.activate();
+    const std::size_t n = std::size_t{dims_} * n_bins_;
+    gpu::upload(ctx, ctx.edges, edges_.data(), n);
+    gpu::upload(ctx, ctx.contrib, contrib.data(), n);
+    gpu::upload(ctx, ctx.lower, lower_.data(), dims_);
+    gpu::upload(ctx, ctx.upper, upper_.data(), dims_);
+    gpu::AdjustArgs a{dims_, n_bins_, ctx.lower.get(), ctx.upper.get(), ctx.edges.get(), ctx.contrib.get(), alpha,
+                      symmetric ? 1 : 0};
+    gpu::launch_adjust(ctx, a);
+    Grid g(*this);
+    gpu::download(ctx, g.edges_.data(), ctx.edges.get(), n);
+    ctx.sync();
+    return g;
+  }
+
+  template <bool kWantBins>
+  double transform_impl(std::span<const double> u, std::span<double> x, std::span<std::uint32_t> bins) const {
+    double jac = 1.0;
+    const double nb = static_cast<double>(n_bins_);
+    for (std::uint32_t j = 0; j < dims_; ++j) {
+      const double z = u[j] * nb;
+      std::uint32_t i = 0;
+      if (z >= nb) i = n_bins_ - 1;
+      else if (z > 0.0) i = static_cast<std::uint32_t>(z);
+      const double* row = edges_.data() + std::size_t{j} * n_bins_;
+      const double left = i == 0 ? lower_[j] : row[i - 1];
+      const double width = row[i] - left;
+      x[j] = left + (z - static_cast<double>(i)) * width;
+      jac *= nb * width;
+      if constexpr (kWantBins) bins[j] = i;
+    }
+    return jac;
+  }
+
+  std::uint32_t dims_;
+  std::uint32_t n_bins_;
+  std::vector<double> lower_;
+  std::vector<double> upper_;
+  std::vector<double> edges_;
+};
+
+// =================================================================== sampler
+/// Unit-space position of a point in cube t (sampler.hpp:75-87).
+inline void cube_unit_point(std::uint64_t t, std::uint64_t g, std::uint32_t dims, std::span<const double> r,
+                            std::span<double> u) {
+  if (g == 0) throw std::invalid_argument("cube_unit_point: g must be >= 1");
+  if (r.size() != dims || u.size() != dims)
+    throw std::invalid_argument("cube_unit_point: r and u must have one entry per axis");
+  std::uint64_t tt = t;
+  const double gd = static_cast<double>(g);
+  for (std::uint32_t j = 0; j < dims; ++j) {
+    u[j] = (static_cast<double>(tt % g) + r[j]) / gd;
+    tt /= g;
+  }
+  if (tt != 0) throw std::invalid_argument("cube_unit_point: cube index out of range");
+}
+
+namespace gpu {
+
+/// One iteration on the GPU for a host grid.  bin_axes: 0 frozen, 1 axis0, d all.
+/// Optional slice [n0, n1) of the linear work index (multi-GPU partition);
+/// words_out (nullable) receives the unrounded exchange words.
+struct SampleResult {
+  double est = 0, var = 0;
+  std::vector<double> contrib;
+};
+
+inline SampleResult sample_once(Context& ctx, const IntegrandOps& ops, const Grid& grid, std::uint64_t m,
+                                std::uint64_t s, std::uint64_t p, std::uint64_t seed, std::uint64_t iteration,
+                                std::uint32_t bin_axes) {
+  ctx.activate();
+  const Shape sh = make_shape(grid.dims(), grid.n_bins(), m, s, p);
+  const std::size_t n = std::size_t{grid.dims()} * grid.n_bins();
+  upload(ctx, ctx.edges, grid.raw_edges().data(), n);
+  upload(ctx, ctx.lower, grid.lowers().data(), grid.dims());
+  unsigned long long* err = ctx.err_key.ensure(1);
+  MCB_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream()));
+  const std::uint64_t root = iteration_key(seed, iteration);
+  const Launch L = ops.k1(ctx, sh, bin_axes, root, 0, m, nullptr, err);
+  unsigned long long* words = ctx.words.ensure(static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords);
+  launch_reduce(ctx, L, bin_axes, sh.nb, words, nullptr);
+  double* sc = ctx.scalars.ensure(2);
+  double* contrib = bin_axes ? ctx.contrib.ensure(n) : nullptr;
+  launch_round(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr);
+  // results back through pinned staging
+  auto* pin = reinterpret_cast<double*>(ctx.pinned());
+  const std::size_t nd = 2 + (bin_axes ? n : 0);
+  if ((nd + 1) * sizeof(double) > Context::kPinnedBytes) throw std::invalid_argument("grid too large");
+  MCB_CUDA(cudaMemcpyAsync(pin, sc, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx.stream()));
+  if (bin_axes) MCB_CUDA(cudaMemcpyAsync(pin + 2, contrib, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream()));
+  MCB_CUDA(cudaMemcpyAsync(pin + nd, err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx.stream()));
+  ctx.sync();
+  unsigned long long key;
+  std::memcpy(&key, pin + nd, sizeof key);
+  if (key != ~0ull) throw_nonfinite(ctx, ops, sh, root, key);
+  SampleResult r;
+  r.est = pin[0];
+  r.var = pin[1];
+  if (bin_axes) r.contrib.assign(pin + 2, pin + 2 + n);
+  return r;
+}
+
+}  // namespace gpu
+
+/// One adjusting iteration (sampler.hpp:312-333), on the GPU.  s and
+/// max_threads are validated/ignored exactly as the reference's outputs are
+/// invariant to them.
+template <gpu::DeviceIntegrand F>
+SampleOutcome v_sample(const F& f, const Grid& grid, std::uint64_t m, std::uint64_t s, std::uint64_t p,
+                       std::uint64_t seed, std::uint64_t iteration, BinUpdate mode = BinUpdate::all_axes,
+                       unsigned max_threads = 0) {
+  (void)max_threads;
+  const std::uint32_t bin_axes = mode == BinUpdate::all_axes ? grid.dims() : 1;
+  auto r = gpu::sample_once(gpu::default_context(), gpu::make_ops(f), grid, m, s, p, seed, iteration, bin_axes);
+  return {r.est, r.var, BinAccumulator(grid.dims(), grid.n_bins(), std::move(r.contrib), m * p * bin_axes)};
+}
+
+/// Frozen-grid iteration (sampler.hpp:339-349), on the GPU.
+template <gpu::DeviceIntegrand F>
+EstimateVariance v_sample_no_adjust(const F& f, const Grid& grid, std::uint64_t m, std::uint64_t s, std::uint64_t p,
+                                    std::uint64_t seed, std::uint64_t iteration, unsigned max_threads = 0) {
+  (void)max_threads;
+  auto r = gpu::sample_once(gpu::default_context(), gpu::make_ops(f), grid, m, s, p, seed, iteration, 0);
+  return {r.est, r.var};
+}
+
+// ==================================================================== driver
+enum class Variant : std::uint8_t { mcubes, mcubes1d };
+
+[[nodiscard]] inline std::string_view variant_name(Variant v) { return v == Variant::mcubes ? "mcubes" : "mcubes1d"; }
+[[nodiscard]] inline std::optional<Variant> parse_variant(std::string_view s) {
+  if (s == "mcubes") return Variant::mcubes;
+  if (s == "mcubes1d") return Variant::mcubes1d;
+  return std::nullopt;
+}
+
+/// driver.hpp:37-71, plus B200 fields at the end (aggregate order preserved).
+struct RunConfig {
+  std::uint32_t dims = 0;
+  std::uint32_t n_bins = 50;
+  std::uint64_t maxcalls = 0;
+  std::uint32_t itmax = 15;
+  std::uint32_t ita = 10;
+  double tau_rel = 1e-3;
+  double alpha = 1.5;
+  double chi2_dof_max = 1.5;
+  std::uint64_t seed = 0;
+  Variant variant = Variant::mcubes;
+  std::vector<double> lower;
+  std::vector<double> upper;
+  unsigned workers = 0;  ///< accepted for source compatibility; the GPU path ignores it
+  gpu::RngKind rng = gpu::RngKind::compat;
+
+  void validate() const {
+    if (dims < 1) throw std::invalid_argument("RunConfig: dims must be >= 1");
+    if (n_bins < 2) throw std::invalid_argument("RunConfig: n_bins must be >= 2");
+    if (dims >= 63 || maxcalls < (std::uint64_t{2} << dims))
+      throw std::invalid_argument("RunConfig: maxcalls must be >= 2*2^dims");
+    if (!(tau_rel > 0.0) || !(tau_rel < 1.0)) throw std::invalid_argument("RunConfig: tau_rel must lie in (0, 1)");
+    if (itmax < 1) throw std::invalid_argument("RunConfig: itmax must be >= 1");
+    if (ita > itmax) throw std::invalid_argument("RunConfig: ita must not exceed itmax");
+    if (!(alpha >= 0.0) || !std::isfinite(alpha)) throw std::invalid_argument("RunConfig: alpha must be finite and >= 0");
+    if (!(chi2_dof_max > 0.0)) throw std::invalid_argument("RunConfig: chi2_dof_max must be positive");
+    if (lower.size() != dims || upper.size() != dims)
+      throw std::invalid_argument("RunConfig: bounds must have one entry per axis");
+    for (std::uint32_t j = 0; j < dims; ++j)
+      if (!std::isfinite(lower[j]) || !std::isfinite(upper[j]) || !(lower[j] < upper[j]))
+        throw std::invalid_argument("RunConfig: requires finite lower < upper on every axis");
+  }
+};
+
+struct SetupParams {
+  std::uint64_t g;
+  std::uint64_t m;
+  std::uint64_t p;
+  std::uint64_t s;
+};
+
+/// driver.hpp:82-87
+[[nodiscard]] inline std::uint64_t set_batch_size(std::uint64_t m, unsigned workers) {
+  if (m == 0) throw std::invalid_argument("set_batch_size: m must be >= 1");
+  if (workers == 0) throw std::invalid_argument("set_batch_size: workers must be >= 1");
+  const std::uint64_t per = std::uint64_t{workers} * 32;
+  return std::max<std::uint64_t>(1, (m + per - 1) / per);
+}
+
+namespace detail {
+/// Largest g with 2*g^d <= maxcalls (driver.hpp:93-108).
+inline std::uint64_t intervals_per_axis(std::uint64_t maxcalls, std::uint32_t d) {
+  const auto fits = [&](std::uint64_t g) {
+    unsigned __int128 acc = 2;
+    for (std::uint32_t i = 0; i < d; ++i) {
+      acc *= g;
+      if (acc > maxcalls) return false;
+    }
+    return true;
+  };
+  auto g = static_cast<std::uint64_t>(
+      std::floor(std::pow(static_cast<double>(maxcalls) / 2.0, 1.0 / static_cast<double>(d))));
+  if (g < 1) g = 1;
+  while (!fits(g) && g > 1) --g;
+  while (fits(g + 1)) ++g;
+  return g;
+}
+}  // namespace detail
+
+/// driver.hpp:114-123
+[[nodiscard]] inline SetupParams setup(const RunConfig& cfg) {
+  cfg.validate();
+  const std::uint64_t g = detail::intervals_per_axis(cfg.maxcalls, cfg.dims);
+  std::uint64_t m = 1;
+  for (std::uint32_t i = 0; i < cfg.dims; ++i) m *= g;
+  const std::uint64_t p = std::max<std::uint64_t>(2, cfg.maxcalls / m);
+  unsigned workers = cfg.workers ? cfg.workers : std::thread::hardware_concurrency();
+  if (workers == 0) workers = 1;
+  return {g, m, p, set_batch_size(m, workers)};
+}
+
+struct IterationResult {
+  double estimate;
+  double variance;
+  std::uint32_t index;
+};
+
+struct Combined {
+  double estimate;
+  double sigma;
+  double chi2_dof;
+};
+
+/// driver.hpp:146-169 (host form; the device form is gpu::weighted_estimate_dev).
+[[nodiscard]] inline Combined weighted_estimate(std::span<const IterationResult> history) {
+  if (history.empty()) throw std::invalid_argument("weighted_estimate: history must be non-empty");
+  for (const IterationResult& it : history)
+    if (!(it.variance >= 0.0)) throw std::invalid_argument("weighted_estimate: negative variance");
+  std::vector<double> e, v;
+  for (const IterationResult& it : history) {
+    e.push_back(it.estimate);
+    v.push_back(it.variance);
+  }
+  Combined c{};
+  gpu::weighted_estimate_dev(e.data(), v.data(), static_cast<std::uint32_t>(e.size()), c.estimate, c.sigma, c.chi2_dof);
+  return c;
+}
+
+/// driver.hpp:173-178
+[[nodiscard]] inline bool check_convergence(const Combined& c, const RunConfig& cfg) {
+  return gpu::converged_dev(c.estimate, c.sigma, c.chi2_dof, cfg.tau_rel, cfg.chi2_dof_max);
+}
+
+struct IntegrationResult {
+  double estimate = 0.0;
+  double sigma = 0.0;
+  double chi2_dof = 0.0;
+  std::uint32_t iterations_used = 0;
+  bool converged = false;
+  std::uint64_t total_samples = 0;
+  std::uint64_t bin_writes = 0;
+  SetupParams params{};
+  std::vector<IterationResult> history;
+};
+
+struct IterationView {
+  std::uint32_t iteration;
+  bool adjusting;
+  const IterationResult& result;
+  const Combined& running;
+  const Grid& grid;
+  std::uint64_t bin_writes;
+};
+
+using IterationObserver = std::function<void(const IterationView&)>;
+
+namespace gpu {
+
+/// A device-resident integrate() run that can be stepped one iteration at a
+/// time -- the multi-GPU driver inserts its all-reduce of exchange_words()
+/// between sample() and finish().  integrate() below is the single-GPU loop.
+class Run {
+ public:
+  Run(Context& ctx, IntegrandOps ops, const RunConfig& cfg) : ctx_(ctx), ops_(std::move(ops)), cfg_(cfg) {
+    sp_ = setup(cfg_);
+    sh_ = make_shape(cfg_.dims, cfg_.n_bins, sp_.m, sp_.s, sp_.p);
+    ctx_.activate();
+    const Grid g0(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper);
+    const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
+    upload(ctx_, ctx_.edges, g0.raw_edges().data(), n);
+    upload(ctx_, ctx_.lower, cfg_.lower.data(), cfg_.dims);
+    upload(ctx_, ctx_.upper, cfg_.upper.data(), cfg_.dims);
+    ctx_.contrib.ensure(n);
+    ctx_.hist_est.ensure(cfg_.itmax);
+    ctx_.hist_var.ensure(cfg_.itmax);
+    MCB_CUDA(cudaMemsetAsync(ctx_.state.ensure(1), 0, sizeof(RunState), ctx_.stream()));
+    MCB_CUDA(cudaMemsetAsync(ctx_.err_key.ensure(1), 0xff, sizeof(unsigned long long), ctx_.stream()));
+    words_ = ctx_.words.ensure(exchange_words(cfg_.dims));
+  }
+
+  const SetupParams& params() const { return sp_; }
+  const Shape& shape() const { return sh_; }
+  std::uint32_t bin_axes(std::uint32_t it) const {
+    if (it > cfg_.ita) return 0;
+    return cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims;
+  }
+  /// Exchange buffer length (u64 words) for the largest (adjusting) iteration.
+  std::size_t exchange_words(std::uint32_t) const {
+    return static_cast<std::size_t>(exchange_accs(cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims, cfg_.n_bins)) *
+           kXWords;
+  }
+  std::size_t exchange_words_for(std::uint32_t it) const {
+    return static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
+  }
+  unsigned long long* exchange() const { return words_; }
+  /// Use a caller-owned exchange buffer (e.g. a torch tensor the caller all-reduces).
+  void set_exchange(unsigned long long* p) { words_ = p ? p : ctx_.words.get(); }
+  const int* stop_flag() const { return &ctx_.state.get()->stop; }
+
+  /// K1 + K3a over the work slice [n0, n1) (default: all cubes).
+  void sample(std::uint32_t it, std::uint64_t n0 = 0, std::uint64_t n1 = ~0ull) {
+    if (n1 > sh_.m) n1 = sh_.m;
+    const std::uint32_t ba = bin_axes(it);
+    const Launch L = ops_.k1(ctx_, sh_, ba, iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get());
+    launch_reduce(ctx_, L, ba, sh_.nb, words_, stop_flag());
+  }
+
+  /// K3b + K4 for iteration it (after the optional all-reduce of exchange()).
+  void finish(std::uint32_t it) {
+    const std::uint32_t ba = bin_axes(it);
+    launch_round(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
+                 ba ? ctx_.contrib.get() : nullptr, stop_flag());
+    EpilogueArgs e{};
+    e.st = ctx_.state.get();
+    e.hist_est = ctx_.hist_est.get();
+    e.hist_var = ctx_.hist_var.get();
+    e.err_key = ctx_.err_key.get();
+    e.it = it;
+    e.adjusting = ba ? 1 : 0;
+    e.tau = cfg_.tau_rel;
+    e.chi2max = cfg_.chi2_dof_max;
+    e.adj = AdjustArgs{cfg_.dims, cfg_.n_bins, ctx_.lower.get(), ctx_.upper.get(), ctx_.edges.get(),
+                       ctx_.contrib.get(), cfg_.alpha, cfg_.variant == Variant::mcubes1d ? 1 : 0};
+    launch_epilogue(ctx_, e);
+  }
+
+  RunState state() {
+    RunState st;
+    MCB_CUDA(cudaMemcpyAsync(&st, ctx_.state.get(), sizeof st, cudaMemcpyDeviceToHost, ctx_.stream()));
+    ctx_.sync();
+    return st;
+  }
+
+  Grid grid() {
+    const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
+    std::vector<double> e(n);
+    download(ctx_, e.data(), ctx_.edges.get(), n);
+    ctx_.sync();
+    return Grid::from_edges(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper, std::move(e));
+  }
+
+  /// Collect the result (one synchronisation); throws NonFiniteSample.
+  IntegrationResult result() {
+    const RunState st = state();
+    IntegrationResult res;
+    res.params = sp_;
+    if (st.failed) {
+      unsigned long long key;
+      MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
+      ctx_.sync();
+      throw_nonfinite(ctx_, ops_, sh_, iteration_key(cfg_.seed, st.failed_iteration), key);
+    }
+    const std::uint32_t n = st.iterations_used;
+    std::vector<double> e(n), v(n);
+    if (n) {
+      download(ctx_, e.data(), ctx_.hist_est.get(), n);
+      download(ctx_, v.data(), ctx_.hist_var.get(), n);
+      ctx_.sync();
+    }
+    for (std::uint32_t i = 0; i < n; ++i) {
+      res.history.push_back({e[i], v[i], i + 1});
+      res.total_samples += sp_.m * sp_.p;
+      res.bin_writes += sp_.m * sp_.p * bin_axes(i + 1);
+    }
+    res.iterations_used = n;
+    res.converged = st.converged != 0;
+    res.estimate = st.estimate;
+    res.sigma = st.sigma;
+    res.chi2_dof = st.chi2_dof;
+    return res;
+  }
+
+ private:
+  Context& ctx_;
+  IntegrandOps ops_;
+  RunConfig cfg_;
+  SetupParams sp_{};
+  Shape sh_{};
+  unsigned long long* words_ = nullptr;
+};
+
+/// integrate() for type-erased integrands: the whole schedule is enqueued
+/// without host synchronisation unless an observer wants per-iteration views.
+inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, const RunConfig& cfg,
+                                       const IterationObserver& observe = {}) {
+  Run run(ctx, ops, cfg);
+  for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
+    run.sample(it);
+    run.finish(it);
+    if (observe) {
+      const RunState st = run.state();
+      if (st.failed || st.iterations_used != it) break;
+      const IterationResult r = run.result().history.back();
+      const Combined c{st.estimate, st.sigma, st.chi2_dof};
+      const Grid g = run.grid();
+      observe(IterationView{it, it <= cfg.ita, r, c, g, run.params().m * run.params().p * run.bin_axes(it)});
+      if (st.stop) break;
+    }
+  }
+  return run.result();
+}
+
+}  // namespace gpu
+
+/// The full integration loop (driver.hpp:215-258), on the GPU.
+template <gpu::DeviceIntegrand F>
+IntegrationResult integrate(const F& f, const RunConfig& cfg, const IterationObserver& observe = {}) {
+  gpu::Context& ctx = gpu::default_context();
+  if (cfg.rng == gpu::RngKind::philox)
+    return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::philox>(f), cfg, observe);
+  return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::compat>(f), cfg, observe);
+}
+
+}  // namespace mcubes

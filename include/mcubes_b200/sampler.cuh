@@ -1,0 +1,269 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K1: the m-Cubes sampling kernel (V-Sample / V-Sample-No-Adjust).
+//
+// Replaces run_cube + sample_all_cubes (sampler.hpp:147-181, 213-278) and the
+// paper's atomics-based CUDA V-Sample.  Design:
+//
+//  * Persistent grid, one 512-thread block per SM.  Work is a range [n0, n1) of
+//    a linear index n; cube t = n*A mod m with A = 1 + g + ... + g^(d-1)
+//    (a bijection because A = 1 mod g).  Neighbouring lanes therefore sit in
+//    cubes whose digits differ by one on EVERY axis, which spreads their bin
+//    deposits over distinct shared-memory words.  Digits advance per thread by
+//    an odometer add of the constant step (T*A mod m), so the per-cube 64-bit
+//    div/mod chain of sampler.hpp:152-158 runs once per thread, not per cube.
+//  * The grid (right edges with the left boundary prepended) lives in shared
+//    memory.
+//  * Per sample, the compat path reproduces the reference arithmetic exactly:
+//    SplitMix keyed stream, (digit + r) / g, the bin map and jacobian of
+//    grid.hpp:204-224, Welford (sampler.hpp:93-104).  IEEE divisions by the
+//    launch constants g, n and p(p-1) use Markstein's correction with a
+//    correctly rounded reciprocal (q0 = a*y; r = fma(-q0, b, a); q = fma(r, y, q0)),
+//    which returns the correctly rounded quotient -- the same bits as a/b.
+//  * Estimates, variances and the d x n_bins contributions (f*J)^2 are summed
+//    EXACTLY into shared-memory superaccumulators (exact.cuh): no global atomics,
+//    results independent of launch geometry and of how cubes are split across
+//    GPUs, and equal to the reference's ExactSum reductions.
+//  * At the end each block writes its accumulators (plain coalesced stores) as
+//    a per-block partial; K3 (epilogue.cuh) sums the partials.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <span>
+#include <type_traits>
+
+#include "config.cuh"
+#include "exact.cuh"
+#include "integrands.cuh"
+#include "rng.cuh"
+
+namespace mcubes::gpu {
+
+/// Shared-memory Welford reciprocal table length (RN(1/n), n < kRcpSmem).
+inline constexpr int kRcpSmem = 64;
+
+struct SampleArgs {
+  const double* edges;  ///< device, dims x nb right edges (grid.hpp:303 layout)
+  const double* lower;  ///< device, dims
+  std::uint32_t dims, nb;
+  std::uint32_t bin_axes;  ///< 0 = frozen (v_sample_no_adjust), 1 = axis0_only, dims = all_axes
+  std::uint32_t pad0;
+  std::uint64_t m, p, g;
+  double nbd;      ///< double(nb)
+  double gd;       ///< double(g)
+  double rcp_g;    ///< RN(1/g)
+  double scale;    ///< 1.0 / (double(m) * double(p))   (sampler.hpp:293)
+  double pp1;      ///< double(p) * double(p - 1)       (sampler.hpp:178)
+  double rcp_pp1;  ///< RN(1/pp1)
+  std::uint64_t iter_root;  ///< compat: iteration_root(seed, it); philox: the key
+  std::uint64_t n0, n1;     ///< this launch's slice of the linear work index
+  std::uint64_t A;          ///< cube(n) = n*A mod m
+  std::uint64_t stepT;      ///< (gridDim*blockDim*A) mod m
+  std::uint64_t step_digits[kMaxDims];  ///< base-g digits of stepT (axis 0 first)
+  std::uint32_t* partials;  ///< [gridDim][kXWords][nacc] u32
+  unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
+  const int* stop;              ///< nullable; nonzero = run finished, skip
+};
+
+/// Accumulator slots in one block's partial.
+MCB_HD int block_accs(std::uint32_t bin_axes, std::uint32_t nb) {
+  return kScalarAccs * kLaneCopies + static_cast<int>(bin_axes * nb);
+}
+
+/// Dynamic shared memory of K1 for a given shape.
+inline std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes) {
+  const std::size_t edges = sizeof(double) * static_cast<std::size_t>(D) * (nb + 1);
+  const std::size_t rcp = sizeof(double) * kRcpSmem;
+  std::size_t acc = sizeof(std::uint32_t) * static_cast<std::size_t>(block_accs(bin_axes, nb)) * kXWords;
+  acc = (acc + 15) & ~std::size_t{15};
+  return edges + rcp + acc;
+}
+
+/// Correctly rounded a / b given y = RN(1/b) (Markstein).
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, y, q0);
+}
+
+template <int D>
+using DigitT = std::conditional_t<(D <= 2), std::uint64_t, std::uint32_t>;
+
+/// One sample: point, jacobian, bins and f*J of sample k of a cube
+/// (sampler.hpp:163-170 with transform_impl, grid.hpp:204-224).
+/// E = shared-memory edges with the left boundary prepended (row stride nb+1).
+template <class F, int D, RngKind R>
+__device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double* E,
+                                               const double (&dg)[D], std::uint64_t t,
+                                               std::uint64_t croot, std::uint64_t k, double (&x)[D],
+                                               std::uint32_t (&bin)[D], double& fx) {
+  const std::uint32_t nb = a.nb, stride = nb + 1, nbm1 = nb - 1;
+  double r[D];
+  if constexpr (R == RngKind::compat) {
+    const std::uint64_t proot = rng::feed(croot, k);  // rng.hpp:55-58
+#pragma unroll
+    for (int j = 0; j < D; ++j) r[j] = rng::to_unit(rng::feed(proot, static_cast<std::uint64_t>(j)));
+  } else {
+#pragma unroll
+    for (int j = 0; j < D; j += 2) {
+      double r0, r1;
+      rng::philox_pair(a.iter_root, t, static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(j >> 1), r0, r1);
+      r[j] = r0;
+      if (j + 1 < D) r[j + 1] = r1;
+    }
+  }
+  double jac = 1.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    // u_j = (digit_j + r_j) / g  (sampler.hpp:165-166)
+    const double u = div_rn(__dadd_rn(dg[j], r[j]), a.gd, a.rcp_g);
+    // transform_impl (grid.hpp:209-222)
+    const double z = __dmul_rn(u, a.nbd);
+    std::uint32_t i = __double2uint_rz(z);
+    i = i < nbm1 ? i : nbm1;
+    const double* row = E + j * stride;
+    const double left = row[i];
+    const double width = __dsub_rn(row[i + 1], left);
+    x[j] = __dadd_rn(left, __dmul_rn(__dsub_rn(z, static_cast<double>(i)), width));
+    jac = __dmul_rn(jac, __dmul_rn(a.nbd, width));
+    bin[j] = i;
+  }
+  fx = static_cast<double>(f(std::span<const double>(x, D)));
+  return __dmul_rn(fx, jac);
+}
+
+template <class F, int D, RngKind R>
+__global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const SampleArgs a, const F f) {
+  if (a.stop && *a.stop) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const std::uint32_t nb = a.nb;
+  const std::uint32_t stride = nb + 1;
+  double* E = reinterpret_cast<double*>(smem);
+  double* rcp = E + D * stride;
+  std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
+  const int nacc = block_accs(a.bin_axes, nb);
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  {  // zero the accumulators, stage the grid and the Welford reciprocals
+    const int nwords = nacc * kXWords;
+    for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
+    for (int i = tid; i < D * static_cast<int>(stride); i += nt) {
+      const int j = i / static_cast<int>(stride), c = i % static_cast<int>(stride);
+      E[i] = c == 0 ? a.lower[j] : a.edges[static_cast<std::size_t>(j) * nb + (c - 1)];
+    }
+    for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
+  }
+  __syncthreads();
+
+  const int lane = tid & 31;
+  std::uint32_t* est_pos = acc + (0 * kLaneCopies + lane) * kXWords;
+  std::uint32_t* est_neg = acc + (1 * kLaneCopies + lane) * kXWords;
+  std::uint32_t* var_acc = acc + (2 * kLaneCopies + lane) * kXWords;
+  std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
+
+  const std::uint64_t T = static_cast<std::uint64_t>(gridDim.x) * nt;
+  std::uint64_t n = a.n0 + static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
+  if (n < a.n1) {
+    using Dig = DigitT<D>;
+    const Dig g = static_cast<Dig>(a.g);
+    std::uint64_t t =
+        static_cast<std::uint64_t>((static_cast<unsigned __int128>(n % a.m) * a.A) % a.m);
+    Dig dig[D];
+    {
+      std::uint64_t tt = t;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        dig[j] = static_cast<Dig>(tt % a.g);
+        tt /= a.g;
+      }
+    }
+    const std::uint32_t bin_axes = a.bin_axes;
+    for (; n < a.n1; n += T) {
+      double dg[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) dg[j] = static_cast<double>(dig[j]);
+      const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
+      double sum = 0.0, mean = 0.0, m2 = 0.0;
+      for (std::uint64_t k = 0; k < a.p; ++k) {
+        double x[D];
+        std::uint32_t bin[D];
+        double fx;
+        const double fj = sample_point<F, D, R>(a, f, E, dg, t, croot, k, x, bin, fx);
+        if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
+          atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+          continue;
+        }
+        sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
+        // Welford (sampler.hpp:98-103)
+        const std::uint64_t nk = k + 1;
+        const double dd = __dsub_rn(fj, mean);
+        const double q = nk < static_cast<std::uint64_t>(kRcpSmem)
+                             ? div_rn(dd, static_cast<double>(nk), rcp[nk])
+                             : __ddiv_rn(dd, static_cast<double>(nk));
+        mean = __dadd_rn(mean, q);
+        m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
+        if (bin_axes) {  // sampler.hpp:173-176
+          const double sq = __dmul_rn(fj, fj);
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+            if (static_cast<std::uint32_t>(j) < bin_axes)
+              exact::add_shared(bins + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords, sq);
+        }
+      }
+      double var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
+      if (!(var > 0.0)) var = 0.0;
+      exact::add_shared(sum < 0.0 ? est_neg : est_pos, sum);
+      exact::add_shared(var_acc, var);
+
+      // advance to cube (n + T)*A mod m: odometer add of stepT's digits
+      t += a.stepT;
+      if (t >= a.m) t -= a.m;
+      Dig carry = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
+        carry = v >= g ? 1 : 0;
+        dig[j] = carry ? v - g : v;
+      }
+    }
+  }
+  __syncthreads();
+
+  // per-block partial: [block][word][slot], coalesced over slots
+  std::uint32_t* out = a.partials + static_cast<std::size_t>(blockIdx.x) * kXWords * nacc;
+  for (int i = tid; i < nacc * kXWords; i += nt) {
+    const int w = i / nacc, c = i % nacc;
+    out[i] = acc[c * kXWords + w];
+  }
+}
+
+/// Recompute one sample (cube t, sample k) -- used to report the point of a
+/// NonFiniteSample (sampler.hpp:31-48) after the failing iteration.
+template <class F, int D, RngKind R>
+__global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t t, std::uint64_t k,
+                                    double* out_x, double* out_fx) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* E = reinterpret_cast<double*>(smem);
+  const std::uint32_t stride = a.nb + 1;
+  for (std::uint32_t i = threadIdx.x; i < D * stride; i += blockDim.x) {
+    const std::uint32_t j = i / stride, c = i % stride;
+    E[i] = c == 0 ? a.lower[j] : a.edges[static_cast<std::size_t>(j) * a.nb + (c - 1)];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double dg[D];
+  std::uint64_t tt = t;
+  for (int j = 0; j < D; ++j) {
+    dg[j] = static_cast<double>(tt % a.g);
+    tt /= a.g;
+  }
+  double x[D];
+  std::uint32_t bin[D];
+  double fx;
+  sample_point<F, D, R>(a, f, E, dg, t, rng::feed(a.iter_root, t), k, x, bin, fx);
+  for (int j = 0; j < D; ++j) out_x[j] = x[j];
+  *out_fx = fx;
+}
+
+}  // namespace mcubes::gpu
