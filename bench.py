@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 m-Cubes VEGAS iteration (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) there is one process per GPU; rank r samples its slice
+of the linear work index and the exact per-iteration exchange buffer
+(est/var/contribution superaccumulator words, include/mcubes_b200.h
+MCB_XWORDS) is all-reduced over NCCL before every rank finishes the
+iteration identically (grid adaptation + weighted estimate on device).
+
+One "step" = one full adjusting m-Cubes iteration (V-Sample K1, exact
+cross-block reduction K3a, [all-reduce], rounding K3b, grid adaptation +
+weighted estimate + convergence gate K4) of 8D Genz f4 (Gaussian) at
+maxcalls = 1e10 (m = 16^8 = 2^32 sub-cubes, p = 2: 8.59e9 integrand evals per
+step).  value = evals/s over the whole job, device-timed with CUDA events, max
+over ranks; L2 is flushed (256 MiB write) between timed steps.
+
+--impl reference runs the reference CPU library (oracle/_ref/libmcubes_ref.so,
+compiled from /root/reference's own headers) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "integrand evals/sec (m-Cubes adjusting iteration, 8D Genz f4)"
+UNIT = "evals/s"
+DIMS = 8
+FAMILY = 4
+MAXCALLS = 10 ** 10
+N_BINS = 50
+# Algorithmic FP64 ops per eval (SURVEY.md 8d convention: +-*/ = 1, exp = 20):
+# map 10d + accumulate (9 + 1 + bin_axes) + integrand f4 (3d + 21).
+OPS_PER_EVAL = 10 * DIMS + (9 + 1 + DIMS) + (3 * DIMS + 21)  # = 143 for d = 8
+FP64_LANES_PER_SM = 64
+REF_SAMPLE_MAXCALLS = 10 ** 8  # bounded CPU sample (m = 9^8, p = 2: 86.1M evals)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = []
+        reasons = set()
+        smax = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, r[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def ref_v_sample_rate(maxcalls: int, steps: int, warmup: int, threads: int, seed0: int = 0):
+    """Time the reference's own v_sample (oracle/_ref) on `threads` host cores."""
+    import numpy as np  # noqa: F401
+    import oracle as O
+
+    lower, upper = [0.0] * DIMS, [1.0] * DIMS
+    sp = (O._U64 * 4)()
+    lib = O.ref()
+    rc = lib.ref_setup(DIMS, N_BINS, maxcalls, 15, 10, 1e-3, 1.5, 1.5, O.darr(lower), O.darr(upper), threads, sp)
+    assert rc == 0, lib.ref_last_error()
+    m, p = sp[1], sp[2]
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.v_sample("ref", FAMILY, None, DIMS, N_BINS, lower, upper, None, m, sp[3], p, seed0, it + 1, "all", threads)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    total = sum(times)
+    return m * p * len(times) / total, m, p, total
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmcubes_ref.so not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    rate, m, p, total = ref_v_sample_rate(REF_SAMPLE_MAXCALLS, args.steps, args.warmup, threads)
+    sample = (f"reference v_sample (oracle/_ref, compiled from /root/reference headers) on 8D f4 at "
+              f"maxcalls=1e8 (m={m}, p={p}: {m * p} evals/step), {threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (keyed RNG stream, no inputs)",
+        "config": {"workload": "8D Genz f4 adjusting iteration", "dims": DIMS, "n_bins": N_BINS,
+                   "maxcalls": REF_SAMPLE_MAXCALLS, "m": m, "p": p, "integrand": "f4"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2202_01753_b200 as M
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # a dedicated (non-default) stream: the library, the CUDA events, the L2
+    # flush and NCCL all order on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+
+    ctx = M.Context(local_rank)
+    ctx.set_stream(stream.cuda_stream)
+    f = M.make_suite_integrand(FAMILY, DIMS)
+    total_its = args.warmup + args.steps
+    cfg = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
+                      tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS)
+    run = M.Run(f, cfg, ctx)
+    sp = M.setup(cfg)
+    m, p = sp.m, sp.p
+    n0, n1 = rank * m // world, (rank + 1) * m // world
+    xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
+    run.set_exchange(xbuf.data_ptr())
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(it, k1_events=None):
+        if k1_events:
+            k1_events[0].record(stream)
+        run.sample(it, n0, n1)
+        if k1_events:
+            k1_events[1].record(stream)
+        run.reduce(it)
+        if dist is not None:
+            dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
+        run.finish(it)
+
+    # warm-up (also compiles/loads everything)
+    for it in range(1, args.warmup + 1):
+        step(it)
+        flush.zero_()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    for i in range(args.steps):
+        it = args.warmup + 1 + i
+        ev[i][0].record(stream)
+        step(it, k1[i])
+        ev[i][1].record(stream)
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    clk = clocks.stop() if clocks else None
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    k1_ms = [a.elapsed_time(b) for a, b in k1]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    res = run.result()
+    assert res.iterations_used == total_its and np.isfinite(res.estimate), res
+
+    evals_per_step = m * p
+    value = evals_per_step * args.steps / (total_ms * 1e-3)
+
+    # ---- end to end through the C ABI with host buffers (H2D grid in, D2H result out)
+    host_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
+    host_edges[:] = run.grid().raw_edges
+    cfg2 = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
+                       tau_rel=1e-15, seed=1, lower=[0.0] * DIMS, upper=[1.0] * DIMS)
+    run2 = M.Run(f, cfg2, ctx)
+    run2.set_exchange(xbuf.data_ptr())
+    out_edges = np.zeros(DIMS * N_BINS)
+
+    def e2e_step(it):
+        run2.set_grid(host_edges)                # H2D: the step's input grid
+        run2.sample(it, n0, n1)
+        run2.reduce(it)
+        if dist is not None:
+            dist.all_reduce(xbuf)
+        run2.finish(it)
+        run2.grid_into(out_edges)                # D2H: adapted grid (synchronises)
+
+    for it in range(1, args.warmup + 1):
+        e2e_step(it)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(args.warmup + 1 + i)
+    e2e_s = time.perf_counter() - t0
+    r2 = run2.result()  # D2H of estimate/variance history
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = evals_per_step * args.steps / e2e_s
+
+    # ---- roofline of the dominant kernel (K1 vsample_kernel)
+    k1_avg_s = 1e-3 * statistics.mean(k1_ms)
+    k1_evals = (n1 - n0) * p
+    achieved_tflops = OPS_PER_EVAL * k1_evals / k1_avg_s / 1e12
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak_tflops = sms * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
+    traffic = None
+    tf_path = os.path.join(HERE, "profiles", "k1_traffic.json")
+    if os.path.exists(tf_path):
+        try:
+            traffic = json.load(open(tf_path)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (keyed SplitMix stream of the reference; no input data)",
+        "config": {"workload": "8D Genz f4 adjusting m-Cubes iteration", "integrand": "f4", "dims": DIMS,
+                   "n_bins": N_BINS, "maxcalls": args.maxcalls, "m": m, "p": p, "evals_per_step": evals_per_step,
+                   "parallelism": f"cube-range partition x{world} + exact all-reduce" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) between timed steps", "rng": "compat (reference SplitMix)",
+                   "reductions": "exact (superaccumulator)"},
+        "clocks": clk,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * DIMS * N_BINS,
+                "d2h_bytes_per_step": 8 * DIMS * N_BINS,
+                "path": "C ABI mcb_run_set_grid/sample/reduce/finish/grid (host grid in, host grid out)"},
+        "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                     "frac": achieved_tflops / peak_tflops, "traffic": traffic,
+                     "kernel": "vsample_kernel<F4,8,compat>", "kernel_ms": 1e3 * k1_avg_s,
+                     "ops_per_eval": OPS_PER_EVAL,
+                     "peak_source": f"FP64 issue: {sms} SMs x {FP64_LANES_PER_SM} lanes x {sm_max:.0f} MHz "
+                                    "(MEASURED_PEAKS.json has no FP64 figure; profiles/microbench_r01.txt "
+                                    "measures 1.75e13 DADD/s)",
+                     "share_of_step": 1e3 * k1_avg_s * args.steps / sum(step_ms)},
+        "result": {"estimate": res.estimate, "sigma": res.sigma, "chi2_dof": res.chi2_dof,
+                   "truth": f.reference},
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline()
+        line["time_to_epsrel"] = time_to_epsrel(M, ctx)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    run.close()
+    run2.close()
+    return 0
+
+
+def cpu_baseline():
+    import oracle as O
+
+    if not O.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    rate, m, p, total = ref_v_sample_rate(REF_SAMPLE_MAXCALLS, 2, 1, threads, seed0=7)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"2 timed reference v_sample iterations of 8D f4 at maxcalls=1e8 (m={m}, p={p}), "
+                      f"{threads} threads, {total:.2f} s"}
+
+
+def time_to_epsrel(M, ctx):
+    """Time-to-target-relative-error (BASELINE metric, config 2) for 8D f5 at
+    tau_rel 1e-3: GPU integrate() vs the reference integrate() on host cores."""
+    import oracle as O
+    import torch
+
+    d, maxcalls, tau = 8, 10 ** 7, 1e-3
+    cfg = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
+                      upper=[1.0] * d)
+    f = M.make_suite_integrand(5, d)
+    M.integrate(f, cfg, ctx=ctx)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = M.integrate(f, cfg, ctx=ctx)
+    gpu_ms = 1e3 * (time.perf_counter() - t0)
+    out = {"integrand": "f5", "dims": d, "maxcalls": maxcalls, "tau_rel": tau, "itmax": 30, "ita": 10, "seed": 1,
+           "gpu_ms": gpu_ms, "gpu_iterations": r.iterations_used, "gpu_converged": r.converged,
+           "gpu_estimate": r.estimate, "gpu_sigma": r.sigma}
+    if O.ref_available():
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        o = O.integrate("ref", 5, None, d, 50, maxcalls, 30, 10, tau, 1.5, 1.5, 1, 0, [0.0] * d, [1.0] * d,
+                        workers=threads)
+        out.update(cpu_ms=1e3 * (time.perf_counter() - t0), cpu_iterations=o["iterations_used"],
+                   cpu_converged=o["converged"], cpu_estimate=o["estimate"], cpu_sigma=o["sigma"],
+                   cpu_threads=threads)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--maxcalls", type=int, default=MAXCALLS)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup < 3 is not allowed by the timing rules; using 3")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -191,9 +191,15 @@ int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
 void* mcb_run_exchange_ptr(const mcb_run* run);
 /* Total linear work items (= m cubes). */
 uint64_t mcb_run_work_items(const mcb_run* run);
+/* K1: sample work items [n0, n1) of iteration it. */
 int mcb_run_sample(mcb_run* run, uint32_t it, uint64_t n0, uint64_t n1);
+/* K3a: exact cross-block sum into the exchange buffer (all-reduce it next). */
+int mcb_run_reduce(mcb_run* run, uint32_t it);
+/* K3b + K4: round, adapt the grid, combine, convergence gate. */
 int mcb_run_finish(mcb_run* run, uint32_t it);
 int mcb_run_result(mcb_run* run, mcb_result* result, mcb_iteration* history, uint32_t history_cap);
+/* Replace the device grid with host edges (dims*n_bins); stream-ordered. */
+int mcb_run_set_grid(mcb_run* run, const double* edges);
 /* Current grid edges (dims*n_bins) -- synchronises. */
 int mcb_run_grid(mcb_run* run, double* edges);
 

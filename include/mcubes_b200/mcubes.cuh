@@ -628,12 +628,17 @@ class Run {
   void set_exchange(unsigned long long* p) { words_ = p ? p : ctx_.words.get(); }
   const int* stop_flag() const { return &ctx_.state.get()->stop; }
 
-  /// K1 + K3a over the work slice [n0, n1) (default: all cubes).
+  /// K1 over the work slice [n0, n1) of the linear work index (default: all cubes).
   void sample(std::uint32_t it, std::uint64_t n0 = 0, std::uint64_t n1 = ~0ull) {
     if (n1 > sh_.m) n1 = sh_.m;
-    const std::uint32_t ba = bin_axes(it);
-    const Launch L = ops_.k1(ctx_, sh_, ba, iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get());
-    launch_reduce(ctx_, L, ba, sh_.nb, words_, stop_flag());
+    last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get());
+    last_it_ = it;
+  }
+
+  /// K3a: this device's per-block partials -> exchange words.
+  void reduce(std::uint32_t it) {
+    if (it != last_it_) throw std::invalid_argument("reduce: iteration was not sampled");
+    launch_reduce(ctx_, last_, bin_axes(it), sh_.nb, words_, stop_flag());
   }
 
   /// K3b + K4 for iteration it (after the optional all-reduce of exchange()).
@@ -660,6 +665,11 @@ class Run {
     MCB_CUDA(cudaMemcpyAsync(&st, ctx_.state.get(), sizeof st, cudaMemcpyDeviceToHost, ctx_.stream()));
     ctx_.sync();
     return st;
+  }
+
+  /// Replace the device grid with host edges (dims*n_bins), stream-ordered.
+  void set_grid(const double* host_edges) {
+    upload(ctx_, ctx_.edges, host_edges, std::size_t{cfg_.dims} * cfg_.n_bins);
   }
 
   Grid grid() {
@@ -708,6 +718,8 @@ class Run {
   SetupParams sp_{};
   Shape sh_{};
   unsigned long long* words_ = nullptr;
+  Launch last_{};
+  std::uint32_t last_it_ = 0;
 };
 
 /// integrate() for type-erased integrands: the whole schedule is enqueued
@@ -717,6 +729,7 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
   Run run(ctx, ops, cfg);
   for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
     run.sample(it);
+    run.reduce(it);
     run.finish(it);
     if (observe) {
       const RunState st = run.state();

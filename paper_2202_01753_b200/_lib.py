@@ -86,8 +86,10 @@ SIGNATURES = {
     "mcb_run_exchange_ptr": (_VP, [_VP]),
     "mcb_run_work_items": (_U64, [_VP]),
     "mcb_run_sample": (C.c_int, [_VP, _U32, _U64, _U64]),
+    "mcb_run_reduce": (C.c_int, [_VP, _U32]),
     "mcb_run_finish": (C.c_int, [_VP, _U32]),
     "mcb_run_result": (C.c_int, [_VP, C.POINTER(mcb_result), C.POINTER(mcb_iteration), _U32]),
+    "mcb_run_set_grid": (C.c_int, [_VP, _PD]),
     "mcb_run_grid": (C.c_int, [_VP, _PD]),
 }
 

@@ -355,6 +355,11 @@ int mcb_run_sample(mcb_run* r, uint32_t it, uint64_t n0, uint64_t n1) {
   });
 }
 
+int mcb_run_reduce(mcb_run* r, uint32_t it) {
+  if (!r) return MCB_EINVAL;
+  return guarded(r->owner, [&] { r->run->reduce(it); });
+}
+
 int mcb_run_finish(mcb_run* r, uint32_t it) {
   if (!r) return MCB_EINVAL;
   return guarded(r->owner, [&] {
@@ -366,6 +371,11 @@ int mcb_run_finish(mcb_run* r, uint32_t it) {
 int mcb_run_result(mcb_run* r, mcb_result* result, mcb_iteration* history, uint32_t cap) {
   if (!r) return MCB_EINVAL;
   return guarded(r->owner, [&] { fill_result(r->run->result(), result, history, cap); });
+}
+
+int mcb_run_set_grid(mcb_run* r, const double* edges) {
+  if (!r || !edges) return MCB_EINVAL;
+  return guarded(r->owner, [&] { r->run->set_grid(edges); });
 }
 
 int mcb_run_grid(mcb_run* r, double* edges) {

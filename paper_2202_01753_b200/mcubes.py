@@ -770,8 +770,26 @@ class Run:
     def sample(self, it: int, n0: int = 0, n1: int = (1 << 64) - 1):
         _raise(self._lib.mcb_run_sample(self.ptr, it, n0, n1), self.ctx.ptr, self.cfg.dims)
 
+    def reduce(self, it: int):
+        _raise(self._lib.mcb_run_reduce(self.ptr, it), self.ctx.ptr, self.cfg.dims)
+
     def finish(self, it: int):
         _raise(self._lib.mcb_run_finish(self.ptr, it), self.ctx.ptr, self.cfg.dims)
+
+    def step(self, it: int):
+        """One whole iteration on this device (sample, reduce, finish)."""
+        self.sample(it)
+        self.reduce(it)
+        self.finish(it)
+
+    def set_grid(self, edges: np.ndarray):
+        """Replace the device grid (stream-ordered H2D copy of dims*n_bins edges)."""
+        _raise(self._lib.mcb_run_set_grid(self.ptr, _dptr(edges)), self.ctx.ptr)
+
+    def grid_into(self, out: np.ndarray):
+        """D2H copy of the current edges into ``out`` (synchronises)."""
+        _raise(self._lib.mcb_run_grid(self.ptr, _dptr(out)), self.ctx.ptr)
+        return out
 
     def grid(self) -> Grid:
         e = np.zeros(self.cfg.dims * self.cfg.n_bins)
