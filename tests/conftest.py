@@ -54,3 +54,17 @@ def ctx():
     import paper_2202_01753_b200 as M
 
     return M.Context(0)
+
+
+def words_value(words) -> list:
+    """Exact integers denoted by an exchange buffer ([accumulator][MCB_XWORDS]
+    radix-2^32 digit sums).  Different partitions carry between words at
+    different points, so compare VALUES, not word vectors."""
+    a = np.asarray(words).astype(np.uint64).reshape(-1, 67)
+    out = []
+    for row in a:
+        v = 0
+        for i in range(66, -1, -1):
+            v = (v << 32) + int(row[i])
+        out.append(v)
+    return out

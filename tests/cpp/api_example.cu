@@ -51,7 +51,7 @@ int main() {
   const auto out = mcubes::v_sample(Seven{}, g, 16, 1, 4, 9, 1);
   const auto g2 = g.adjusted(out.contributions, 1.5);
   std::printf("VSAMPLE estimate %.17g variance %.17g writes %llu edge %.17g\n", out.raw_estimate, out.raw_variance,
-              static_cast<unsigned long long>(out.contributions.writes()), g2.edges(0)[3]);
+              static_cast<unsigned long long>(out.contributions.writes()), g2.edges(0)[7]);
   try {
     (void)mcubes::v_sample(Bad{}, g, 16, 1, 4, 9, 1);
     std::printf("NONFINITE none\n");
