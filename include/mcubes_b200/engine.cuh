@@ -245,7 +245,7 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
   a.gd = static_cast<double>(sh.g);
   a.rcp_g = sh.rcp_g;
   a.iter_root = iter_root;
-  const std::size_t smem = sizeof(double) * D * (sh.nb + 1);
+  const std::size_t smem = 2 * sizeof(double) * D * sh.nb;
   auto kern = sample_point_kernel<F, D, R>;
   MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<1, 128, smem, ctx.stream()>>>(a, f, t, k, out_x, out_fx);

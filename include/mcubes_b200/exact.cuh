@@ -64,6 +64,61 @@ MCB_HD bool split(double v, Digits& out) {
 }
 
 #ifdef __CUDACC__
+/// Rare tail of a deposit: a carry out of the third word ripples upward.
+template <int kTag = 0>
+__device__ __noinline__ void carry_up(std::uint32_t* p, std::uint32_t* end) {
+  for (; p < end; ++p)
+    if (atomicAdd(p, 1u) != 0xffffffffu) break;
+}
+
+/// Add pre-split digits at p = acc + dg.w (three word atomics, carries
+/// travel through the returned old values).  Branch-free except for the
+/// ~2^-11-probability ripple out of the top word.
+__device__ __forceinline__ void add_digits(std::uint32_t* p, std::uint32_t* end, const Digits& dg) {
+  const std::uint32_t o0 = atomicAdd(p, dg.d0);
+  const std::uint32_t c0 = (o0 + dg.d0) < o0 ? 1u : 0u;
+  const std::uint32_t t1 = dg.d1 + c0;  // wraps to 0 only if d1 == 0xffffffff and c0
+  const std::uint32_t o1 = atomicAdd(p + 1, t1);
+  const std::uint32_t c1 = ((t1 < c0) || ((o1 + t1) < o1)) ? 1u : 0u;
+  const std::uint32_t t2 = dg.d2 + c1;  // d2 < 2^21: never wraps
+  const std::uint32_t o2 = atomicAdd(p + 2, t2);
+  if ((o2 + t2) < o2) carry_up(p + 3, end);
+}
+
+/// Deposit the same digits into N accumulators (one per axis) -- the
+/// sampler's bin update, where every axis receives the same (f J)^2
+/// (sampler.hpp:173-176).  The atomics are issued word-major across the N
+/// accumulators, so a sample pays three shared-memory round trips instead of
+/// 3N, and the rare ripple out of the top word is one check per sample.
+/// p[j] = accumulator j + dg.w.
+template <int N>
+__device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::uint32_t* end, const Digits& dg) {
+  std::uint32_t c[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t o = atomicAdd(p[j], dg.d0);
+    c[j] = (o + dg.d0) < o ? 1u : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t t = dg.d1 + c[j];  // wraps to 0 only if d1 == 0xffffffff and a carry in
+    const std::uint32_t o = atomicAdd(p[j] + 1, t);
+    c[j] = static_cast<std::uint32_t>(t < c[j]) | static_cast<std::uint32_t>((o + t) < o);
+  }
+  std::uint32_t ripple = 0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t t = dg.d2 + c[j];  // d2 < 2^21: never wraps
+    const std::uint32_t o = atomicAdd(p[j] + 2, t);
+    ripple |= static_cast<std::uint32_t>((o + t) < o) << j;
+  }
+  if (ripple) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if ((ripple >> j) & 1u) carry_up(p[j] + 3, end);
+  }
+}
+
 /// Add |v| exactly into a shared-memory accumulator of kXWords u32 words.
 /// Carries travel through the atomics' returned old values, so concurrent
 /// deposits from any lanes/warps compose to the exact total.

@@ -73,11 +73,11 @@ MCB_HD int block_accs(std::uint32_t bin_axes, std::uint32_t nb) {
 
 /// Dynamic shared memory of K1 for a given shape.
 inline std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes) {
-  const std::size_t edges = sizeof(double) * static_cast<std::size_t>(D) * (nb + 1);
+  const std::size_t grid = 2 * sizeof(double) * static_cast<std::size_t>(D) * nb;  // {left, width}
   const std::size_t rcp = sizeof(double) * kRcpSmem;
   std::size_t acc = sizeof(std::uint32_t) * static_cast<std::size_t>(block_accs(bin_axes, nb)) * kXWords;
   acc = (acc + 15) & ~std::size_t{15};
-  return edges + rcp + acc;
+  return grid + rcp + acc;
 }
 
 /// Correctly rounded a / b given y = RN(1/b) (Markstein).
@@ -90,15 +90,27 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
 template <int D>
 using DigitT = std::conditional_t<(D <= 2), std::uint64_t, std::uint32_t>;
 
+/// Stage the grid as per-bin {left edge, width} pairs (one 128-bit LDS per
+/// axis per sample).  width = right - left exactly as grid.hpp:218-219.
+template <int D>
+__device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
+  const std::uint32_t nb = a.nb;
+  for (std::uint32_t idx = threadIdx.x; idx < D * nb; idx += blockDim.x) {
+    const std::uint32_t j = idx / nb, i = idx % nb;
+    const double* row = a.edges + static_cast<std::size_t>(j) * nb;
+    const double left = i == 0 ? a.lower[j] : row[i - 1];
+    LW[idx] = make_double2(left, __dsub_rn(row[i], left));
+  }
+}
+
 /// One sample: point, jacobian, bins and f*J of sample k of a cube
 /// (sampler.hpp:163-170 with transform_impl, grid.hpp:204-224).
-/// E = shared-memory edges with the left boundary prepended (row stride nb+1).
 template <class F, int D, RngKind R>
-__device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double* E,
+__device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double2* LW,
                                                const double (&dg)[D], std::uint64_t t,
-                                               std::uint64_t croot, std::uint64_t k, double (&x)[D],
+                                               std::uint64_t croot, std::uint32_t k, double (&x)[D],
                                                std::uint32_t (&bin)[D], double& fx) {
-  const std::uint32_t nb = a.nb, stride = nb + 1, nbm1 = nb - 1;
+  const std::uint32_t nb = a.nb, nbm1 = nb - 1;
   double r[D];
   if constexpr (R == RngKind::compat) {
     const std::uint64_t proot = rng::feed(croot, k);  // rng.hpp:55-58
@@ -108,7 +120,7 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
 #pragma unroll
     for (int j = 0; j < D; j += 2) {
       double r0, r1;
-      rng::philox_pair(a.iter_root, t, static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(j >> 1), r0, r1);
+      rng::philox_pair(a.iter_root, t, k, static_cast<std::uint32_t>(j >> 1), r0, r1);
       r[j] = r0;
       if (j + 1 < D) r[j + 1] = r1;
     }
@@ -122,11 +134,9 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
     const double z = __dmul_rn(u, a.nbd);
     std::uint32_t i = __double2uint_rz(z);
     i = i < nbm1 ? i : nbm1;
-    const double* row = E + j * stride;
-    const double left = row[i];
-    const double width = __dsub_rn(row[i + 1], left);
-    x[j] = __dadd_rn(left, __dmul_rn(__dsub_rn(z, static_cast<double>(i)), width));
-    jac = __dmul_rn(jac, __dmul_rn(a.nbd, width));
+    const double2 lw = LW[j * nb + i];
+    x[j] = __dadd_rn(lw.x, __dmul_rn(__dsub_rn(z, static_cast<double>(i)), lw.y));
+    jac = __dmul_rn(jac, __dmul_rn(a.nbd, lw.y));
     bin[j] = i;
   }
   fx = static_cast<double>(f(std::span<const double>(x, D)));
@@ -138,9 +148,8 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   if (a.stop && *a.stop) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const std::uint32_t nb = a.nb;
-  const std::uint32_t stride = nb + 1;
-  double* E = reinterpret_cast<double*>(smem);
-  double* rcp = E + D * stride;
+  double2* LW = reinterpret_cast<double2*>(smem);
+  double* rcp = reinterpret_cast<double*>(LW + D * nb);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
   const int nacc = block_accs(a.bin_axes, nb);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -148,10 +157,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   {  // zero the accumulators, stage the grid and the Welford reciprocals
     const int nwords = nacc * kXWords;
     for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
-    for (int i = tid; i < D * static_cast<int>(stride); i += nt) {
-      const int j = i / static_cast<int>(stride), c = i % static_cast<int>(stride);
-      E[i] = c == 0 ? a.lower[j] : a.edges[static_cast<std::size_t>(j) * nb + (c - 1)];
-    }
+    stage_grid<D>(LW, a);
     for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
   }
   __syncthreads();
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   std::uint32_t* est_neg = acc + (1 * kLaneCopies + lane) * kXWords;
   std::uint32_t* var_acc = acc + (2 * kLaneCopies + lane) * kXWords;
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
+  std::uint32_t* const acc_end = acc + nacc * kXWords;
 
   const std::uint64_t T = static_cast<std::uint64_t>(gridDim.x) * nt;
   std::uint64_t n = a.n0 + static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
@@ -179,36 +186,44 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
       }
     }
     const std::uint32_t bin_axes = a.bin_axes;
+    const std::uint32_t p = static_cast<std::uint32_t>(a.p);
     for (; n < a.n1; n += T) {
       double dg[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) dg[j] = static_cast<double>(dig[j]);
       const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
       double sum = 0.0, mean = 0.0, m2 = 0.0;
-      for (std::uint64_t k = 0; k < a.p; ++k) {
+      for (std::uint32_t k = 0; k < p; ++k) {
         double x[D];
         std::uint32_t bin[D];
         double fx;
-        const double fj = sample_point<F, D, R>(a, f, E, dg, t, croot, k, x, bin, fx);
+        const double fj = sample_point<F, D, R>(a, f, LW, dg, t, croot, k, x, bin, fx);
         if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
           continue;
         }
         sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
         // Welford (sampler.hpp:98-103)
-        const std::uint64_t nk = k + 1;
+        const std::uint32_t nk = k + 1;
         const double dd = __dsub_rn(fj, mean);
-        const double q = nk < static_cast<std::uint64_t>(kRcpSmem)
-                             ? div_rn(dd, static_cast<double>(nk), rcp[nk])
-                             : __ddiv_rn(dd, static_cast<double>(nk));
+        const double q = nk < static_cast<std::uint32_t>(kRcpSmem) ? div_rn(dd, static_cast<double>(nk), rcp[nk])
+                                                                   : __ddiv_rn(dd, static_cast<double>(nk));
         mean = __dadd_rn(mean, q);
         m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
-        if (bin_axes) {  // sampler.hpp:173-176
-          const double sq = __dmul_rn(fj, fj);
+        if (bin_axes) {  // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once
+          exact::Digits dgt;
+          if (exact::split(__dmul_rn(fj, fj), dgt)) {
+            std::uint32_t* const base = bins + dgt.w;
+            if (bin_axes == static_cast<std::uint32_t>(D)) {
+              std::uint32_t* ptrs[D];
 #pragma unroll
-          for (int j = 0; j < D; ++j)
-            if (static_cast<std::uint32_t>(j) < bin_axes)
-              exact::add_shared(bins + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords, sq);
+              for (int j = 0; j < D; ++j) ptrs[j] = base + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords;
+              exact::add_digits_n<D>(ptrs, acc_end, dgt);
+            } else {  // BinUpdate::axis0_only
+              std::uint32_t* const ptrs[1] = {base + bin[0] * kXWords};
+              exact::add_digits_n<1>(ptrs, acc_end, dgt);
+            }
+          }
         }
       }
       double var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
@@ -244,12 +259,8 @@ template <class F, int D, RngKind R>
 __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t t, std::uint64_t k,
                                     double* out_x, double* out_fx) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* E = reinterpret_cast<double*>(smem);
-  const std::uint32_t stride = a.nb + 1;
-  for (std::uint32_t i = threadIdx.x; i < D * stride; i += blockDim.x) {
-    const std::uint32_t j = i / stride, c = i % stride;
-    E[i] = c == 0 ? a.lower[j] : a.edges[static_cast<std::size_t>(j) * a.nb + (c - 1)];
-  }
+  double2* LW = reinterpret_cast<double2*>(smem);
+  stage_grid<D>(LW, a);
   __syncthreads();
   if (threadIdx.x != 0) return;
   double dg[D];
@@ -261,7 +272,7 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
   double x[D];
   std::uint32_t bin[D];
   double fx;
-  sample_point<F, D, R>(a, f, E, dg, t, rng::feed(a.iter_root, t), k, x, bin, fx);
+  sample_point<F, D, R>(a, f, LW, dg, t, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
   for (int j = 0; j < D; ++j) out_x[j] = x[j];
   *out_fx = fx;
 }
