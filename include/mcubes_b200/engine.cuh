@@ -128,6 +128,7 @@ class Context {
     device_ = device;
     MCB_CUDA(cudaSetDevice(device_));
     MCB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_));
+    MCB_CUDA(cudaDeviceGetAttribute(&max_smem_, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
     MCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
     stream_ = own_stream_;
     MCB_CUDA(cudaMallocHost(&pinned_, kPinnedBytes));
@@ -142,6 +143,7 @@ class Context {
 
   int device() const { return device_; }
   int sms() const { return sms_; }
+  int max_smem() const { return max_smem_; }
   cudaStream_t stream() const { return stream_; }
   /// Run on a caller-owned stream (e.g. torch's current stream) instead.
   void set_stream(cudaStream_t s) { stream_ = s ? s : own_stream_; }
@@ -152,9 +154,11 @@ class Context {
   std::uint64_t launches = 0;
 
   DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var, scalars, point;
-  DevBuf<std::uint32_t> partials;
+  DevBuf<std::uint32_t> partials;            ///< K1 bin partials [block][word][slot]
+  DevBuf<unsigned long long> scal_partials;  ///< K1 est+/est-/var partials [block][kind][word]
   DevBuf<unsigned long long> words, err_key;
   DevBuf<RunState> state;
+  DevBuf<unsigned int> counter;  ///< finish-kernel last-block counter (self-resetting)
   DevBuf<double> table;  ///< parameters of a stateful integrand (owned copy)
 
   static constexpr std::size_t kPinnedBytes = 1 << 20;
@@ -163,6 +167,7 @@ class Context {
  private:
   int device_ = 0;
   int sms_ = 0;
+  int max_smem_ = 0;
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t stream_ = nullptr;
   unsigned char* pinned_ = nullptr;
@@ -181,15 +186,20 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   auto kern = vsample_kernel<F, D, R>;
   Launch L;
   L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
-  int max_smem = 0;
-  MCB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx.device()));
-  if (L.smem > static_cast<std::size_t>(max_smem))
+  if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
     throw std::invalid_argument("B200 path: dims*n_bins too large for the shared-memory histogram (" +
-                                std::to_string(L.smem) + " B > " + std::to_string(max_smem) + " B)");
-  MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
-  int occ = 0;
-  MCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSampleThreads, L.smem));
-  occ = std::max(occ, 1);
+                                std::to_string(L.smem) + " B > " + std::to_string(ctx.max_smem()) + " B)");
+  // attribute + occupancy queries are cached per instantiation (host latency
+  // matters for small-ncall iterations)
+  thread_local std::size_t cached_smem = 0;
+  thread_local int cached_occ = 0, cached_dev = -1;
+  if (cached_smem != L.smem || cached_dev != ctx.device()) {
+    MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
+    MCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_occ, kern, kSampleThreads, L.smem));
+    cached_smem = L.smem;
+    cached_dev = ctx.device();
+  }
+  const int occ = std::max(cached_occ, 1);
   const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
   const std::uint64_t want = (work + kSampleThreads - 1) / kSampleThreads;
   L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
@@ -220,8 +230,8 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
     a.step_digits[j] = j < static_cast<int>(sh.dims) ? st % sh.g : 0;
     if (j < static_cast<int>(sh.dims)) st /= sh.g;
   }
-  const int nacc = block_accs(bin_axes, sh.nb);
-  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * nacc);
+  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * (bin_axes * sh.nb) + 1);
+  a.scal_partials = ctx.scal_partials.ensure(static_cast<std::size_t>(L.blocks) * kScalarAccs * kXWords);
   a.err_key = err_key;
   a.stop = stop;
   kern<<<L.blocks, kSampleThreads, L.smem, ctx.stream()>>>(a, f);
@@ -293,20 +303,38 @@ void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t ite
   throw std::invalid_argument("B200 path: no kernel compiled for dims=" + std::to_string(sh.dims));
 }
 
-/// K3a: per-block partials -> exchange words (zeroing the scalar slots first).
+/// K3a: per-block partials -> exchange words (zeroed first; chunks of blocks
+/// meet in exact 64-bit integer atomics).
 inline void launch_reduce(Context& ctx, const Launch& L, std::uint32_t bin_axes, std::uint32_t nb,
                           unsigned long long* words, const int* stop) {
-  const int nacc = block_accs(bin_axes, nb);
-  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * kScalarAccs * kXWords, ctx.stream()));
-  const int n = nacc * kXWords;
-  reduce_partials_kernel<0><<<(n + 255) / 256, 256, 0, ctx.stream()>>>(ctx.partials.get(), L.blocks, nacc, words, stop);
+  const int nbins = static_cast<int>(bin_axes * nb);
+  const int n = (nbins + kScalarAccs) * kXWords;
+  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * n, ctx.stream()));
+  const int chunks = std::max(1, std::min(L.blocks, 16));
+  const dim3 grid((n + 255) / 256, chunks);
+  reduce_partials_kernel<0><<<grid, 256, 0, ctx.stream()>>>(ctx.partials.get(), ctx.scal_partials.get(), L.blocks,
+                                                             nbins, words, stop);
   MCB_CUDA(cudaGetLastError());
   ++ctx.launches;
 }
 
-/// K3b: exchange words -> estimate, variance, contributions.
-inline void launch_round(Context& ctx, const Shape& sh, std::uint32_t bin_axes, const unsigned long long* words,
-                         double* est, double* var, double* contrib, const int* stop) {
+/// Warps of a finish/adjust block that adapt axes (one axis each); their
+/// scratch bounds the block's shared memory.
+inline int adjust_warps(std::uint32_t dims, std::uint32_t nb, int max_smem) {
+  int w = std::max(1, std::min<int>(static_cast<int>(dims), kFinishThreads / 32));
+  const std::size_t fixed = sizeof(double) * static_cast<std::size_t>(dims) * nb;
+  while (w > 1 && fixed + sizeof(double) * static_cast<std::size_t>(w) * kAdjustScratch * nb >
+                      static_cast<std::size_t>(max_smem))
+    --w;
+  if (fixed + sizeof(double) * static_cast<std::size_t>(w) * kAdjustScratch * nb > static_cast<std::size_t>(max_smem))
+    throw std::invalid_argument("B200 path: n_bins too large for the on-device grid adaptation");
+  return w;
+}
+
+/// K3b + K4 fused: exchange words -> estimate, variance, contributions; with
+/// an epilogue, also grid adaptation + weighted estimate + convergence.
+inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes, const unsigned long long* words,
+                          double* est, double* var, double* contrib, const int* stop, const EpilogueArgs* epi) {
   RoundArgs r{};
   r.words = words;
   r.dims = sh.dims;
@@ -317,37 +345,40 @@ inline void launch_round(Context& ctx, const Shape& sh, std::uint32_t bin_axes, 
   r.var = var;
   r.contrib = contrib;
   r.stop = stop;
-  const int n = static_cast<int>(sh.dims * sh.nb + 2);
-  round_kernel<0><<<(n + 127) / 128, 128, 0, ctx.stream()>>>(r);
+  EpilogueArgs e{};
+  std::size_t smem = 0;
+  if (epi) {
+    e = *epi;
+    e.adj_warps = adjust_warps(sh.dims, sh.nb, ctx.max_smem());
+    smem = sizeof(double) *
+           (static_cast<std::size_t>(sh.dims) * sh.nb + static_cast<std::size_t>(e.adj_warps) * kAdjustScratch * sh.nb);
+  }
+  thread_local std::size_t attr_smem = 0;
+  if (smem > 48 * 1024 && smem > attr_smem) {
+    MCB_CUDA(cudaFuncSetAttribute(finish_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_smem = smem;
+  }
+  unsigned int* counter = ctx.counter.get();
+  if (!counter) {
+    counter = ctx.counter.ensure(1);
+    MCB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx.stream()));
+  }
+  const int values = static_cast<int>(sh.dims * sh.nb + 2);  // one warp per output value
+  const int warps_per_block = kFinishThreads / 32;
+  finish_kernel<0><<<(values + warps_per_block - 1) / warps_per_block, kFinishThreads, smem, ctx.stream()>>>(
+      r, e, epi ? 1 : 0, counter);
   MCB_CUDA(cudaGetLastError());
   ++ctx.launches;
-}
-
-inline int adjust_threads(std::uint32_t dims, int symmetric) {
-  const int warps = symmetric ? 4 : std::max<int>(1, std::min<int>(static_cast<int>(dims), 16));
-  return 32 * warps;
-}
-
-inline std::size_t adjust_smem(int threads, std::uint32_t nb) {
-  return sizeof(double) * static_cast<std::size_t>(threads / 32) * 3 * nb;
 }
 
 /// Standalone Grid::adjusted on device (edges in ctx.edges, contributions in
 /// ctx.contrib).
-inline void launch_adjust(Context& ctx, const AdjustArgs& a) {
-  const int th = adjust_threads(a.dims, a.symmetric);
-  const std::size_t smem = adjust_smem(th, a.nb);
-  MCB_CUDA(cudaFuncSetAttribute(adjust_grid_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  adjust_grid_kernel<0><<<1, th, smem, ctx.stream()>>>(a);
-  MCB_CUDA(cudaGetLastError());
-  ++ctx.launches;
-}
-
-inline void launch_epilogue(Context& ctx, const EpilogueArgs& e) {
-  const int th = adjust_threads(e.adj.dims, e.adj.symmetric);
-  const std::size_t smem = adjust_smem(th, e.adj.nb);
-  MCB_CUDA(cudaFuncSetAttribute(epilogue_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  epilogue_kernel<0><<<1, th, smem, ctx.stream()>>>(e);
+inline void launch_adjust(Context& ctx, AdjustArgs a) {
+  const int w = adjust_warps(a.dims, a.nb, ctx.max_smem());
+  const std::size_t smem = sizeof(double) * static_cast<std::size_t>(w) * kAdjustScratch * a.nb;
+  if (smem > 48 * 1024)
+    MCB_CUDA(cudaFuncSetAttribute(adjust_grid_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  adjust_grid_kernel<0><<<1, 32 * w, smem, ctx.stream()>>>(a);
   MCB_CUDA(cudaGetLastError());
   ++ctx.launches;
 }

@@ -1,17 +1,18 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// K3 (cross-block exact reduction + rounding) and K4 (on-device grid
-// adaptation, inverse-variance combination, chi^2 and the convergence gate).
-// Together with K1 they make one m-Cubes iteration with no host round trip.
+// K3a (cross-block exact reduction) and the fused "finish" kernel K3b+K4
+// (exact rounding, on-device grid adaptation, inverse-variance combination,
+// chi^2 and the convergence gate).  Together with K1 they make one m-Cubes
+// iteration with no host round trip.
 //
 // K3a sums the per-block partials into the exchange buffer (unnormalised u64
 // digit sums -- integer, so exact and order-free; under multi-GPU this buffer
-// is what NCCL all-reduces).  K3b rounds each accumulator to the nearest
-// double exactly like ExactSum::value() (exact_sum.hpp:137-179) and produces
-// v_sample's outputs (sampler.hpp:322-332).  K4 replaces Grid::adjusted /
-// adjusted_symmetric (grid.hpp:104-146, 232-297), weighted_estimate and
-// check_convergence (driver.hpp:146-178) and the loop bookkeeping of integrate
-// (driver.hpp:227-256).
+// is what NCCL all-reduces).  The finish kernel rounds each accumulator to
+// the nearest double exactly like ExactSum::value() (exact_sum.hpp:137-179),
+// producing v_sample's outputs (sampler.hpp:322-332), then replaces
+// Grid::adjusted / adjusted_symmetric (grid.hpp:104-146, 232-297),
+// weighted_estimate and check_convergence (driver.hpp:146-178) and the loop
+// bookkeeping of integrate (driver.hpp:227-256).
 #pragma once
 
 #include <cmath>
@@ -39,75 +40,73 @@ MCB_HD int exchange_accs(std::uint32_t bin_axes, std::uint32_t nb) {
 }
 
 // ------------------------------------------------------------------ K3a
+/// Per-block partial layouts written by K1:
+///   bins    [block][word][slot]  u32 digits (slot = axis*nb + bin), coalesced over slots
+///   scalars [block][kind][word]  u64 sums of the 32 lane copies (kind = est+, est-, var)
+/// K3a sums them over blocks into the exchange buffer (zeroed beforehand).
+/// Blocks are split into `gridDim.y` chunks whose sums meet in 64-bit integer
+/// atomics: integer addition, so exact and order-free.
 template <int kTag = 0>
-__global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ partials, int nblocks,
-                                       int nacc, unsigned long long* __restrict__ words,
+__global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ bins, const unsigned long long* __restrict__ scal,
+                                       int nblocks, int nbins, unsigned long long* __restrict__ words,
                                        const int* stop) {
   if (stop && *stop) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // = w * nacc + c
-  if (idx >= nacc * kXWords) return;
-  const int w = idx / nacc, c = idx % nacc;
-  const std::size_t bstride = static_cast<std::size_t>(kXWords) * nacc;
-  unsigned long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-  int b = 0;
-  for (; b + 4 <= nblocks; b += 4) {
-    s0 += partials[(b + 0) * bstride + idx];
-    s1 += partials[(b + 1) * bstride + idx];
-    s2 += partials[(b + 2) * bstride + idx];
-    s3 += partials[(b + 3) * bstride + idx];
-  }
-  for (; b < nblocks; ++b) s0 += partials[b * bstride + idx];
-  const unsigned long long s = s0 + s1 + s2 + s3;
-  const int lanes = kScalarAccs * kLaneCopies;
-  if (c < lanes) {
-    if (s) atomicAdd(words + (c / kLaneCopies) * kXWords + w, s);  // integer: order-free
-  } else {
-    words[(kScalarAccs + (c - lanes)) * kXWords + w] = s;
-  }
-}
-
-// ------------------------------------------------------------------ K3b
-struct RoundArgs {
-  const unsigned long long* words;  ///< [exchange_accs][kXWords]
-  std::uint32_t dims, nb, bin_axes;
-  double md2;        ///< double(m) * double(m)  (sampler.hpp:330-331)
-  double* est;       ///< 1 double
-  double* var;       ///< 1 double
-  double* contrib;   ///< dims*nb (nullable for frozen iterations)
-  const int* stop;
-};
-
-template <int kTag = 0>
-__global__ void round_kernel(const RoundArgs a) {
-  if (a.stop && *a.stop) return;
-  const int total = static_cast<int>(a.dims * a.nb);
-  const int nbins = static_cast<int>(a.bin_axes * a.nb);
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < total + 2; c += gridDim.x * blockDim.x) {
-    if (c == total) {
-      *a.est = exact::round_words(a.words, a.words + kXWords);
-    } else if (c == total + 1) {
-      *a.var = exact::round_words(a.words + 2 * kXWords, nullptr) / a.md2;
-    } else if (a.contrib) {
-      a.contrib[c] = c < nbins ? exact::round_words(a.words + (kScalarAccs + c) * kXWords, nullptr) : 0.0;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nbin_words = nbins * kXWords, nscal_words = kScalarAccs * kXWords;
+  if (idx >= nbin_words + nscal_words) return;
+  const int chunk = (nblocks + gridDim.y - 1) / gridDim.y;
+  const int b0 = blockIdx.y * chunk, b1 = min(nblocks, b0 + chunk);
+  unsigned long long s0 = 0, s1 = 0;
+  if (idx < nbin_words) {  // idx = w * nbins + c
+    const std::size_t stride = static_cast<std::size_t>(nbin_words);
+    int b = b0;
+    for (; b + 2 <= b1; b += 2) {
+      s0 += bins[(b + 0) * stride + idx];
+      s1 += bins[(b + 1) * stride + idx];
     }
+    if (b < b1) s0 += bins[b * stride + idx];
+    const unsigned long long s = s0 + s1;
+    const int w = idx / nbins, c = idx % nbins;
+    if (s) atomicAdd(words + (kScalarAccs + c) * kXWords + w, s);
+  } else {  // idx - nbin_words = kind * kXWords + w
+    const int j = idx - nbin_words;
+    for (int b = b0; b < b1; ++b) s0 += scal[static_cast<std::size_t>(b) * nscal_words + j];
+    if (s0) atomicAdd(words + j, s0);
   }
 }
 
-// ------------------------------------------------------------------ K4 pieces
-/// adjust_axis (grid.hpp:232-297) by one warp: the element-wise steps
-/// (smoothing, ((c-1)/ln c)^alpha) run lane-parallel, every running sum and
-/// the rebinning walk run on lane 0 in the reference's order.
-/// scratch: 3*n doubles.  contrib must be finite and >= 0 (checked by callers).
-__device__ inline void adjust_axis_warp(double* edges, double lo, double hi, const double* contrib,
+// ------------------------------------------------------------------ grid adaptation
+/// adjust_axis (grid.hpp:232-297) by one warp, in shared memory.
+///
+/// The reference's rebinning walk is sequential; here it is reformulated so
+/// every output edge is found in parallel with exactly the reference's
+/// floating-point values:
+///   * the running sums the walk accumulates -- cum after each old bin,
+///     P[k+1] = RN(P[k] + imp[k]), and the targets T[i] = RN(T[i-1] + share)
+///     -- are computed sequentially by lane 0 in the reference's order;
+///   * the walk stops output i at the first k with imp[k] != 0 and
+///     P[k+1] >= T[i] (or n-1).  Because T is non-decreasing, that is the
+///     same k the sequential loop reaches from the previous output's k;
+///   * the edge is left + width * ((T[i] - P[k]) / imp[k]) as in the reference.
+/// The nextafter repair passes run sequentially only if some edge needs one.
+/// scratch: kAdjustScratch * n doubles.  contrib must be finite and >= 0.
+inline constexpr int kAdjustScratch = 6;  ///< doubles per bin of per-warp scratch
+
+__device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, const double* contrib,
                                         std::uint32_t n, double alpha, double* scratch) {
   const int lane = threadIdx.x & 31;
+  double* edges = scratch;
+  double* smooth = scratch + n;
+  double* imp = scratch + 2 * n;
+  double* P = scratch + 3 * n;      // n + 1 entries: cum before bin k
+  double* T = scratch + 4 * n + 1;  // n - 1 targets
   bool any_local = false;
-  for (std::uint32_t i = lane; i < n; i += 32) any_local |= contrib[i] != 0.0;
+  for (std::uint32_t i = lane; i < n; i += 32) {
+    edges[i] = edges_g[i];
+    any_local |= contrib[i] != 0.0;
+  }
   const bool any = __any_sync(0xffffffffu, any_local);
-  if (!any || n == 1) return;
-  double* smooth = scratch;
-  double* imp = scratch + n;
-  double* out = scratch + 2 * n;
+  if (!any || n == 1) return;  // nothing observed: leave the axis alone
   for (std::uint32_t i = lane; i < n; i += 32) {
     double s;
     if (i == 0) s = 0.5 * (contrib[0] + contrib[1]);
@@ -117,8 +116,10 @@ __device__ inline void adjust_axis_warp(double* edges, double lo, double hi, con
   }
   __syncwarp();
   double total = 0.0;
-  if (lane == 0)
+  if (lane == 0) {
+#pragma unroll 8
     for (std::uint32_t i = 0; i < n; ++i) total += smooth[i];
+  }
   total = __shfl_sync(0xffffffffu, total, 0);
   for (std::uint32_t i = lane; i < n; i += 32) {
     const double c = smooth[i] / total;
@@ -128,24 +129,52 @@ __device__ inline void adjust_axis_warp(double* edges, double lo, double hi, con
     imp[i] = r;
   }
   __syncwarp();
-  if (lane == 0) {
-    double rtot = 0.0;
-    for (std::uint32_t i = 0; i < n; ++i) rtot += imp[i];
-    const double share = rtot / static_cast<double>(n);
-    out[n - 1] = hi;
-    double target = 0.0, cum = 0.0;
-    std::uint32_t k = 0;
+  if (lane == 0) {  // the reference's sequential accumulations, in its order
+    // rtot (grid.hpp:603-613) and the walk's cum (grid.hpp:623-626) add the
+    // same imp[] in the same order, so one pass yields both: P[n] == rtot.
+    double cum = 0.0;
+    P[0] = 0.0;
+#pragma unroll 8
+    for (std::uint32_t k = 0; k < n; ++k) {
+      cum += imp[k];
+      P[k + 1] = cum;
+    }
+    const double share = cum / static_cast<double>(n);
+    double target = 0.0;
+#pragma unroll 8
     for (std::uint32_t i = 0; i + 1 < n; ++i) {
       target += share;
-      while (k + 1 < n && (imp[k] == 0.0 || cum + imp[k] < target)) {
-        cum += imp[k];
-        ++k;
-      }
-      const double left = k == 0 ? lo : edges[k - 1];
-      const double width = edges[k] - left;
-      out[i] = left + width * ((target - cum) / imp[k]);
+      T[i] = target;
     }
-    double prev = lo;  // repair passes (grid.hpp:285-294)
+  }
+  __syncwarp();
+  double* out = smooth;  // smooth is dead: reuse it as the output row
+  for (std::uint32_t i = lane; i + 1 < n; i += 32) {
+    const double t = T[i];
+    // first k in [0, n-1) with imp[k] != 0 and P[k+1] >= t, else n-1: binary
+    // search the monotone P for the first P[k+1] >= t, then step over
+    // zero-importance bins (whose P[k+1] == P[k]).
+    std::uint32_t lo_k = 0, hi_k = n - 1;
+    while (lo_k < hi_k) {
+      const std::uint32_t mid = (lo_k + hi_k) >> 1;
+      if (P[mid + 1] < t) lo_k = mid + 1;
+      else hi_k = mid;
+    }
+    std::uint32_t k = lo_k;
+    while (k + 1 < n && (imp[k] == 0.0 || P[k + 1] < t)) ++k;
+    const double left = k == 0 ? lo : edges[k - 1];
+    const double width = edges[k] - left;
+    out[i] = left + width * ((t - P[k]) / imp[k]);
+  }
+  __syncwarp();
+  bool bad = false;
+  for (std::uint32_t i = lane; i + 1 < n; i += 32) {
+    const double prev = i == 0 ? lo : out[i - 1];
+    const double next = i + 2 == n ? hi : out[i + 1];
+    bad |= !(out[i] > prev) || !(out[i] < next);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) {  // repair passes (grid.hpp:285-294)
+    double prev = lo;
     for (std::uint32_t i = 0; i + 1 < n; ++i) {
       if (!(out[i] > prev)) out[i] = nextafter(prev, INFINITY);
       prev = out[i];
@@ -157,7 +186,7 @@ __device__ inline void adjust_axis_warp(double* edges, double lo, double hi, con
     }
   }
   __syncwarp();
-  for (std::uint32_t i = lane; i < n; i += 32) edges[i] = out[i];
+  for (std::uint32_t i = lane; i < n; i += 32) edges_g[i] = i + 1 < n ? out[i] : hi;
   __syncwarp();
 }
 
@@ -169,19 +198,21 @@ struct AdjustArgs {
   const double* contrib;  ///< dims x nb (symmetric: row 0 only is read)
   double alpha;
   int symmetric;
+  double* contrib_scratch;  ///< device dims x nb: finish-kernel staging when no contrib output is kept
 };
 
-/// Grid::adjusted / adjusted_symmetric on device: warp j adapts axis j
-/// (symmetric: warp 0 adapts axis 0, then all warps replicate it).
-/// Dynamic smem: blockDim/32 * 3*nb doubles.
-__device__ inline void adjust_grid_block(const AdjustArgs& a) {
-  extern __shared__ double adj_scratch[];
-  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double* scratch = adj_scratch + static_cast<std::size_t>(warp) * 3 * a.nb;
+/// Grid::adjusted / adjusted_symmetric: warp j adapts axis j (symmetric: warp
+/// 0 adapts axis 0, then all warps replicate it).  `contrib` may point to
+/// shared or global memory.  scratch: nwarps * kAdjustScratch * nb doubles.
+__device__ inline void adjust_grid_block(const AdjustArgs& a, const double* contrib, double* scratch_all,
+                                         int adj_warps) {
+  const int warp = threadIdx.x >> 5;
+  double* scratch = scratch_all + static_cast<std::size_t>(warp) * kAdjustScratch * a.nb;
   const std::uint32_t axes = a.symmetric ? 1u : a.dims;
-  for (std::uint32_t j = warp; j < axes; j += nwarps)
-    adjust_axis_warp(a.edges + static_cast<std::size_t>(j) * a.nb, a.lower[j], a.upper[j],
-                     a.contrib + static_cast<std::size_t>(j) * a.nb, a.nb, a.alpha, scratch);
+  if (warp < adj_warps)
+    for (std::uint32_t j = warp; j < axes; j += adj_warps)
+      adjust_axis_warp(a.edges + static_cast<std::size_t>(j) * a.nb, a.lower[j], a.upper[j],
+                       contrib + static_cast<std::size_t>(j) * a.nb, a.nb, a.alpha, scratch);
   if (!a.symmetric) return;
   __syncthreads();
   const double* row0 = a.edges;
@@ -201,7 +232,10 @@ __device__ inline void adjust_grid_block(const AdjustArgs& a) {
 }
 
 template <int kTag = 0>
-__global__ void adjust_grid_kernel(const AdjustArgs a) { adjust_grid_block(a); }
+__global__ void adjust_grid_kernel(const AdjustArgs a) {
+  extern __shared__ double adj_scratch[];
+  adjust_grid_block(a, a.contrib, adj_scratch, blockDim.x >> 5);
+}
 
 /// weighted_estimate (driver.hpp:146-169) -- IEEE ops in the reference's order.
 MCB_HD void weighted_estimate_dev(const double* est, const double* var, std::uint32_t n, double& mean,
@@ -237,6 +271,17 @@ MCB_HD bool converged_dev(double est, double sigma, double chi2, double tau, dou
   return error_ok && chi2 <= chi2max;
 }
 
+// ------------------------------------------------------------------ finish (K3b + K4)
+struct RoundArgs {
+  const unsigned long long* words;  ///< [exchange_accs][kXWords]
+  std::uint32_t dims, nb, bin_axes;
+  double md2;        ///< double(m) * double(m)  (sampler.hpp:330-331)
+  double* est;       ///< 1 double
+  double* var;       ///< 1 double
+  double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
+  const int* stop;
+};
+
 struct EpilogueArgs {
   RunState* st;
   const double* hist_est;
@@ -244,34 +289,80 @@ struct EpilogueArgs {
   const unsigned long long* err_key;
   std::uint32_t it;  ///< 1-based iteration just sampled
   int adjusting;
+  int adj_warps;  ///< warps with adaptation scratch (set by launch_finish)
   double tau, chi2max;
   AdjustArgs adj;
 };
 
-/// K4: one block; runs after K3b of iteration `it`.
+inline constexpr int kFinishThreads = 512;
+
+/// Phase 1 (all blocks): one warp per output value -- warp-cooperative exact
+/// rounding of the contributions, the estimate and the variance.
+/// Phase 2 (integrate only, the LAST block to finish phase 1): failure check,
+/// grid adaptation (contributions staged in shared memory), weighted
+/// estimate, chi^2/dof and the convergence gate.  `counter` must be 0 at
+/// launch; the last block resets it.
 template <int kTag = 0>
-__global__ void epilogue_kernel(const EpilogueArgs a) {
-  RunState* st = a.st;
-  const int stop0 = st->stop;
-  __syncthreads();  // every thread reads `stop` before thread 0 may set it
+__global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs r, const EpilogueArgs e,
+                                                                int with_epilogue, unsigned int* counter) {
+  extern __shared__ double fin_smem[];
+  __shared__ bool is_last;
+  const int stop0 = r.stop ? *r.stop : 0;
+  __syncthreads();  // every thread reads `stop` before the last block may set it
   if (stop0) return;
-  if (*a.err_key != ~0ull) {  // NonFiniteSample: abort the run (driver.hpp:231-241 propagate)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int total = static_cast<int>(r.dims * r.nb);
+  const int nbins = static_cast<int>(r.bin_axes * r.nb);
+  double* contrib_out = r.contrib ? r.contrib : e.adj.contrib_scratch;
+
+  const int c = blockIdx.x * nwarps + warp;
+  if (c < total + 2) {
+    if (c == total) {
+      const double v = exact::warp_round_words(r.words, r.words + kXWords);
+      if (lane == 0) *r.est = v;
+    } else if (c == total + 1) {
+      const double v = exact::warp_round_words(r.words + 2 * kXWords, nullptr) / r.md2;
+      if (lane == 0) *r.var = v;
+    } else {
+      const double v =
+          c < nbins ? exact::warp_round_words(r.words + static_cast<std::size_t>(kScalarAccs + c) * kXWords, nullptr)
+                    : 0.0;
+      if (lane == 0 && contrib_out) contrib_out[c] = v;
+    }
+  }
+  if (!with_epilogue) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *counter = 0u;
+
+  double* contrib_s = fin_smem;
+  double* scratch = fin_smem + static_cast<std::size_t>(r.dims) * r.nb;
+  if (e.adjusting)
+    for (int i = threadIdx.x; i < total; i += blockDim.x) contrib_s[i] = contrib_out[i];
+  __syncthreads();
+
+  RunState* st = e.st;
+  if (*e.err_key != ~0ull) {  // NonFiniteSample: abort the run (driver.hpp:231-241 propagate)
     if (threadIdx.x == 0) {
       st->failed = 1;
-      st->failed_iteration = a.it;
+      st->failed_iteration = e.it;
       st->stop = 1;
     }
     return;
   }
-  if (a.adjusting) adjust_grid_block(a.adj);
+  if (e.adjusting) adjust_grid_block(e.adj, contrib_s, scratch, e.adj_warps);
   if (threadIdx.x == 0) {
     double mean, sigma, chi2;
-    weighted_estimate_dev(a.hist_est, a.hist_var, a.it, mean, sigma, chi2);
+    weighted_estimate_dev(e.hist_est, e.hist_var, e.it, mean, sigma, chi2);
     st->estimate = mean;
     st->sigma = sigma;
     st->chi2_dof = chi2;
-    st->iterations_used = a.it;
-    if (converged_dev(mean, sigma, chi2, a.tau, a.chi2max)) {
+    st->iterations_used = e.it;
+    if (converged_dev(mean, sigma, chi2, e.tau, e.chi2max)) {
       st->converged = 1;
       st->stop = 1;
     }

@@ -93,29 +93,73 @@ __device__ __forceinline__ void add_digits(std::uint32_t* p, std::uint32_t* end,
 /// p[j] = accumulator j + dg.w.
 template <int N>
 __device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::uint32_t* end, const Digits& dg) {
-  std::uint32_t c[N];
+  // Carry arithmetic in PTX add.cc/addc (SASS: IADD3 with predicate
+  // carry-out / IADD3.X carry-in): per word the carry out of (old + digit)
+  // is folded straight into the next word's addend.
+  std::uint32_t t1[N], u[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const std::uint32_t o = atomicAdd(p[j], dg.d0);
-    c[j] = (o + dg.d0) < o ? 1u : 0u;
+    // t1 = d1 + carry(o + d0); u = d2 + carry(t1 wrapped)   (d2 < 2^21: u never wraps)
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
+        : "=r"(t1[j]), "=r"(u[j])
+        : "r"(o), "r"(dg.d0), "r"(dg.d1), "r"(dg.d2));
   }
+  std::uint32_t t2[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-    const std::uint32_t t = dg.d1 + c[j];  // wraps to 0 only if d1 == 0xffffffff and a carry in
-    const std::uint32_t o = atomicAdd(p[j] + 1, t);
-    c[j] = static_cast<std::uint32_t>(t < c[j]) | static_cast<std::uint32_t>((o + t) < o);
+    const std::uint32_t o = atomicAdd(p[j] + 1, t1[j]);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(t2[j]) : "r"(o), "r"(t1[j]), "r"(u[j]));
   }
-  std::uint32_t ripple = 0;
+  std::uint32_t ripple = 0;  // bit (N-1-j) = carry out of axis j's top word
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-    const std::uint32_t t = dg.d2 + c[j];  // d2 < 2^21: never wraps
-    const std::uint32_t o = atomicAdd(p[j] + 2, t);
-    ripple |= static_cast<std::uint32_t>((o + t) < o) << j;
+    const std::uint32_t o = atomicAdd(p[j] + 2, t2[j]);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t2[j]));
   }
   if (ripple) {
 #pragma unroll
     for (int j = 0; j < N; ++j)
-      if ((ripple >> j) & 1u) carry_up(p[j] + 3, end);
+      if ((ripple >> (N - 1 - j)) & 1u) carry_up(p[j] + 3, end);
+  }
+}
+
+/// Two independent exact adds (the per-cube estimate and variance), issued
+/// interleaved so their atomic round trips overlap.
+__device__ __forceinline__ void add_shared2(std::uint32_t* acc_a, double a, std::uint32_t* acc_b, double b,
+                                            std::uint32_t* end_a, std::uint32_t* end_b) {
+  Digits da, db;
+  const bool ha = split(a, da), hb = split(b, db);
+  if (ha && hb) {
+    std::uint32_t* const pa[1] = {acc_a + da.w};
+    std::uint32_t* const pb[1] = {acc_b + db.w};
+    // the two accumulators receive different digits: interleave by hand
+    std::uint32_t ta, ua, tb, ub;
+    std::uint32_t o = atomicAdd(pa[0], da.d0);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
+        : "=r"(ta), "=r"(ua) : "r"(o), "r"(da.d0), "r"(da.d1), "r"(da.d2));
+    o = atomicAdd(pb[0], db.d0);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
+        : "=r"(tb), "=r"(ub) : "r"(o), "r"(db.d0), "r"(db.d1), "r"(db.d2));
+    o = atomicAdd(pa[0] + 1, ta);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(ta) : "r"(o), "r"(ta), "r"(ua));
+    o = atomicAdd(pb[0] + 1, tb);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(tb) : "r"(o), "r"(tb), "r"(ub));
+    std::uint32_t ra = 0, rb = 0;
+    o = atomicAdd(pa[0] + 2, ta);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t}" : "=r"(ra) : "r"(o), "r"(ta));
+    o = atomicAdd(pb[0] + 2, tb);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t}" : "=r"(rb) : "r"(o), "r"(tb));
+    if (ra | rb) {
+      if (ra) carry_up(pa[0] + 3, end_a);
+      if (rb) carry_up(pb[0] + 3, end_b);
+    }
+  } else if (ha) {
+    std::uint32_t* const pa[1] = {acc_a + da.w};
+    add_digits_n<1>(pa, end_a, da);
+  } else if (hb) {
+    std::uint32_t* const pb[1] = {acc_b + db.w};
+    add_digits_n<1>(pb, end_b, db);
   }
 }
 
@@ -212,6 +256,152 @@ MCB_HD double round_words(const unsigned long long* pos, const unsigned long lon
   }
   return cmp > 0 ? r : -r;
 }
+
+#ifdef __CUDACC__
+namespace warpx {
+// Warp-cooperative exact rounding.  Lane l holds words w = l + 32k, k = 0..2
+// (kXWords = 67 <= 96).  Carries/borrows move up one word per step through
+// shuffles; a step clears all carries unless a run of all-ones words is met,
+// so the loops finish in ~2-3 steps.
+
+__device__ __forceinline__ unsigned long long up1(unsigned long long x0, unsigned long long x1,
+                                                  unsigned long long x2, int k, int lane) {
+  // value of register k from the previous word (w - 1)
+  const unsigned long long src = k == 0 ? x0 : (k == 1 ? x1 : x2);
+  const unsigned long long prev_lane = __shfl_up_sync(0xffffffffu, src, 1);
+  const unsigned long long wrap = __shfl_sync(0xffffffffu, k == 0 ? 0ull : (k == 1 ? x0 : x1), 31);
+  return lane == 0 ? (k == 0 ? 0ull : wrap) : prev_lane;
+}
+
+/// Normalise unsigned digit sums into radix-2^32 digits (v[k] < 2^32).
+__device__ __forceinline__ void normalise(unsigned long long (&v)[3], int lane) {
+  while (true) {
+    unsigned long long c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      c[k] = v[k] >> 32;
+      v[k] &= 0xffffffffull;
+    }
+    const bool any = (c[0] | c[1] | c[2]) != 0;
+    if (!__any_sync(0xffffffffu, any)) return;
+    unsigned long long in[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) in[k] = up1(c[0], c[1], c[2], k, lane);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] += in[k];
+  }
+}
+
+/// a -= b for normalised digits with a >= b.
+__device__ __forceinline__ void subtract(unsigned long long (&a)[3], const unsigned long long (&b)[3], int lane) {
+  long long d[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) d[k] = static_cast<long long>(a[k]) - static_cast<long long>(b[k]);
+  while (true) {
+    unsigned long long br[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      br[k] = d[k] < 0 ? 1ull : 0ull;
+      d[k] += static_cast<long long>(br[k]) << 32;
+    }
+    if (!__any_sync(0xffffffffu, (br[0] | br[1] | br[2]) != 0)) break;
+    unsigned long long in[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) in[k] = up1(br[0], br[1], br[2], k, lane);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] -= static_cast<long long>(in[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) a[k] = static_cast<unsigned long long>(d[k]);
+}
+
+/// Highest word index whose predicate holds (-1 if none); uniform across the warp.
+__device__ __forceinline__ int top_word(bool p0, bool p1, bool p2) {
+  const unsigned m2 = __ballot_sync(0xffffffffu, p2), m1 = __ballot_sync(0xffffffffu, p1),
+                 m0 = __ballot_sync(0xffffffffu, p0);
+  if (m2) return 64 + 31 - __clz(m2);
+  if (m1) return 32 + 31 - __clz(m1);
+  if (m0) return 31 - __clz(m0);
+  return -1;
+}
+
+/// Digit w (uniform) broadcast to all lanes.
+__device__ __forceinline__ unsigned long long digit(const unsigned long long (&v)[3], int w) {
+  if (w < 0) return 0ull;
+  const int k = w >> 5;
+  const unsigned long long x = k == 0 ? v[0] : (k == 1 ? v[1] : v[2]);
+  return __shfl_sync(0xffffffffu, x, w & 31);
+}
+}  // namespace warpx
+
+/// Warp-cooperative form of round_words: RN-even of (pos - neg) * 2^-1074
+/// (ExactSum::value(), exact_sum.hpp:137-179).  All 32 lanes call it; every
+/// lane returns the result.
+__device__ __forceinline__ double warp_round_words(const unsigned long long* pos, const unsigned long long* neg) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long a[3], b[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int w = lane + 32 * k;
+    a[k] = w < kXWords ? pos[w] : 0ull;
+    b[k] = (w < kXWords && neg) ? neg[w] : 0ull;
+  }
+  warpx::normalise(a, lane);
+  bool negative = false;
+  if (neg) {
+    warpx::normalise(b, lane);
+    const int dw = warpx::top_word(a[0] != b[0], a[1] != b[1], a[2] != b[2]);
+    if (dw < 0) return 0.0;
+    if (warpx::digit(a, dw) < warpx::digit(b, dw)) {
+      negative = true;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const unsigned long long t = a[k];
+        a[k] = b[k];
+        b[k] = t;
+      }
+    }
+    warpx::subtract(a, b, lane);
+  }
+  const int tw = warpx::top_word(a[0] != 0, a[1] != 0, a[2] != 0);
+  if (tw < 0) return 0.0;
+  const unsigned long long d2 = warpx::digit(a, tw), d1 = warpx::digit(a, tw - 1), d0 = warpx::digit(a, tw - 2);
+  // any nonzero digit below the 3-word window
+  const int lw = tw - 3;
+  const unsigned below = __ballot_sync(0xffffffffu, (lane <= lw && a[0] != 0) || (lane + 32 <= lw && a[1] != 0) ||
+                                                         (lane + 64 <= lw && a[2] != 0));
+  double r;
+  const int top = 32 * tw + 31 - __clz(static_cast<unsigned>(d2));
+  if (top <= 52) {
+    const unsigned long long v = warpx::digit(a, 0) | (warpx::digit(a, 1) << 32);
+    r = ldexp(static_cast<double>(v), -1074);
+  } else {
+    // 96-bit window X = d2:d1:d0 covering bit positions [32(tw-2), 32(tw+1))
+    const int base = 32 * (tw - 2);
+    const int lo = top - 52 - base;  // window-relative position of the mantissa LSB (may be < 0 if tw < 2)
+    const unsigned __int128 X = (static_cast<unsigned __int128>(d2) << 64) | (static_cast<unsigned __int128>(d1) << 32) | d0;
+    unsigned long long mant;
+    bool guard, sticky = below != 0;
+    if (lo >= 1) {
+      mant = static_cast<unsigned long long>(X >> lo) & ((1ull << 53) - 1);
+      guard = ((X >> (lo - 1)) & 1) != 0;
+      if (lo >= 2) sticky = sticky || (X & ((static_cast<unsigned __int128>(1) << (lo - 1)) - 1)) != 0;
+    } else {  // only when the value is tiny (tw < 2): the whole number is in the window
+      mant = static_cast<unsigned long long>(X >> (lo > 0 ? lo : 0));
+      guard = false;
+    }
+    int e = top - 52 - 1074;
+    if (guard && (sticky || (mant & 1))) {
+      if (++mant == (1ull << 53)) {
+        mant >>= 1;
+        ++e;
+      }
+    }
+    r = ldexp(static_cast<double>(mant), e);
+  }
+  return negative ? -r : r;
+}
+#endif
 
 /// Host-side exact add into exchange-format words (used by host tools/tests).
 inline void add_words(unsigned long long* acc, double v) {

@@ -395,7 +395,7 @@ inline SampleResult sample_once(Context& ctx, const IntegrandOps& ops, const Gri
   launch_reduce(ctx, L, bin_axes, sh.nb, words, nullptr);
   double* sc = ctx.scalars.ensure(2);
   double* contrib = bin_axes ? ctx.contrib.ensure(n) : nullptr;
-  launch_round(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr);
+  launch_finish(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr, nullptr);
   // results back through pinned staging
   auto* pin = reinterpret_cast<double*>(ctx.pinned());
   const std::size_t nd = 2 + (bin_axes ? n : 0);
@@ -641,11 +641,10 @@ class Run {
     launch_reduce(ctx_, last_, bin_axes(it), sh_.nb, words_, stop_flag());
   }
 
-  /// K3b + K4 for iteration it (after the optional all-reduce of exchange()).
+  /// K3b + K4 (one fused kernel) for iteration it, after the optional
+  /// all-reduce of exchange().
   void finish(std::uint32_t it) {
     const std::uint32_t ba = bin_axes(it);
-    launch_round(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
-                 ba ? ctx_.contrib.get() : nullptr, stop_flag());
     EpilogueArgs e{};
     e.st = ctx_.state.get();
     e.hist_est = ctx_.hist_est.get();
@@ -655,9 +654,13 @@ class Run {
     e.adjusting = ba ? 1 : 0;
     e.tau = cfg_.tau_rel;
     e.chi2max = cfg_.chi2_dof_max;
-    e.adj = AdjustArgs{cfg_.dims, cfg_.n_bins, ctx_.lower.get(), ctx_.upper.get(), ctx_.edges.get(),
-                       ctx_.contrib.get(), cfg_.alpha, cfg_.variant == Variant::mcubes1d ? 1 : 0};
-    launch_epilogue(ctx_, e);
+    e.adj = AdjustArgs{cfg_.dims,       cfg_.n_bins,
+                       ctx_.lower.get(), ctx_.upper.get(),
+                       ctx_.edges.get(), ctx_.contrib.get(),
+                       cfg_.alpha,       cfg_.variant == Variant::mcubes1d ? 1 : 0,
+                       ctx_.contrib.get()};
+    launch_finish(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
+                  ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e);
   }
 
   RunState state() {

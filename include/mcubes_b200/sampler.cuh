@@ -61,7 +61,8 @@ struct SampleArgs {
   std::uint64_t A;          ///< cube(n) = n*A mod m
   std::uint64_t stepT;      ///< (gridDim*blockDim*A) mod m
   std::uint64_t step_digits[kMaxDims];  ///< base-g digits of stepT (axis 0 first)
-  std::uint32_t* partials;  ///< [gridDim][kXWords][nacc] u32
+  std::uint32_t* partials;             ///< bins: [gridDim][kXWords][bin_axes*nb] u32
+  unsigned long long* scal_partials;   ///< est+/est-/var: [gridDim][3][kXWords] u64 (lane copies folded)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
 };
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
       }
       double var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
       if (!(var > 0.0)) var = 0.0;
-      exact::add_shared(sum < 0.0 ? est_neg : est_pos, sum);
-      exact::add_shared(var_acc, var);
+      std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
+      exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
 
       // advance to cube (n + T)*A mod m: odometer add of stepT's digits
       t += a.stepT;
@@ -245,11 +246,22 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   }
   __syncthreads();
 
-  // per-block partial: [block][word][slot], coalesced over slots
-  std::uint32_t* out = a.partials + static_cast<std::size_t>(blockIdx.x) * kXWords * nacc;
-  for (int i = tid; i < nacc * kXWords; i += nt) {
-    const int w = i / nacc, c = i % nacc;
-    out[i] = acc[c * kXWords + w];
+  // per-block partials.  Bins: [block][word][slot] u32, coalesced over slots.
+  // Scalars: the 32 lane copies folded into u64 word sums (< 2^37, exact).
+  const int nbins = static_cast<int>(a.bin_axes * nb);
+  std::uint32_t* out = a.partials + static_cast<std::size_t>(blockIdx.x) * kXWords * nbins;
+  for (int i = tid; i < nbins * kXWords; i += nt) {
+    const int w = i / nbins, c = i % nbins;
+    out[i] = bins[c * kXWords + w];
+  }
+  unsigned long long* sout = a.scal_partials + static_cast<std::size_t>(blockIdx.x) * kScalarAccs * kXWords;
+  for (int i = tid; i < kScalarAccs * kXWords; i += nt) {
+    const int kind = i / kXWords, w = i % kXWords;
+    const std::uint32_t* src = acc + kind * kLaneCopies * kXWords + w;
+    unsigned long long s = 0;
+#pragma unroll 8
+    for (int l = 0; l < kLaneCopies; ++l) s += src[l * kXWords];
+    sout[i] = s;
   }
 }
 

@@ -47,7 +47,7 @@ int main(int argc, char** argv) {
   gpu::launch_reduce(ctx, L, D, 50, words, nullptr);
   double* sc = ctx.scalars.ensure(2);
   double* contrib = ctx.contrib.ensure(D * 50);
-  gpu::launch_round(ctx, sh, D, words, sc, sc + 1, contrib, nullptr);
+  gpu::launch_finish(ctx, sh, D, words, sc, sc + 1, contrib, nullptr, nullptr);
   double h[2];
   gpu::download(ctx, h, sc, 2);
   ctx.sync();
