@@ -164,8 +164,9 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2202_01753_b200 as M
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     # a dedicated (non-default) stream: the library, the CUDA events, the L2
     # flush and NCCL all order on it
     stream = torch.cuda.Stream(dev)
@@ -175,7 +176,7 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist_mod
         dist = dist_mod
 
-    ctx = M.Context(local_rank)
+    ctx = M.Context(gpu)
     ctx.set_stream(stream.cuda_stream)
     f = M.make_suite_integrand(FAMILY, DIMS)
     total_its = args.warmup + args.steps
@@ -208,7 +209,7 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
 
-    clocks = ClockSampler(local_rank) if rank == 0 else None
+    clocks = ClockSampler(gpu) if rank == 0 else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
@@ -390,8 +391,15 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        gpu = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        # NCCL over NVLink in production; MCB_DIST_BACKEND=gloo lets several
+        # ranks share one GPU for testing the multi-rank path
+        backend = os.environ.get("MCB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     try:
         return run_ours(args, rank, world, local_rank)
     finally:

@@ -1,0 +1,66 @@
+"""GPU: the real multi-rank path (paper_2202_01753_b200.dist.integrate) with
+two processes.  The round's GPU boxes have one GPU, so both ranks share
+cuda:0 and the exchange buffer (a CUDA int64 tensor) is all-reduced over
+gloo; on an 8xB200 box the same code runs over NCCL.  Every rank must hold
+the same result, bitwise equal to the single-process run."""
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+D, MAXCALLS = 6, 2 * 10 ** 6
+
+
+def _cfg(M):
+    return M.RunConfig(dims=D, maxcalls=MAXCALLS, itmax=6, ita=4, tau_rel=1e-15, seed=13, lower=[0.0] * D,
+                       upper=[1.0] * D)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2202_01753_b200 as M
+        from paper_2202_01753_b200 import dist as mdist
+
+        torch.cuda.set_device(0)
+        r = mdist.integrate(M.make_suite_integrand(4, D), _cfg(M))
+        q.put((rank, r.estimate, r.sigma, r.chi2_dof, [h.estimate for h in r.history],
+               [h.variance for h in r.history]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_integrate_matches_single(world, ctx):
+    import paper_2202_01753_b200 as M
+
+    want = M.integrate(M.make_suite_integrand(4, D), _cfg(M), ctx=ctx)
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, est, sigma, chi2, he, hv in res:
+        assert est == want.estimate and sigma == want.sigma and chi2 == want.chi2_dof
+        assert he == [h.estimate for h in want.history] and hv == [h.variance for h in want.history]
