@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -369,6 +370,87 @@ def time_to_epsrel(M, ctx):
     return out
 
 
+def run_suite(path: str):
+    """BASELINE.json configs 1-5 beside the reference CPU library (oracle/_ref,
+    all host threads), one JSON line per measurement, written to `path`.
+    Bounded: CPU legs stop at 1e8-1e9 evals."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    import paper_2202_01753_b200 as M
+
+    ctx = M.Context(0)
+    threads = os.cpu_count() or 1
+    out = open(path, "w")
+
+    def emit(d):
+        line = json.dumps(d, default=lambda x: x.item() if hasattr(x, "item") else str(x))
+        out.write(line + "\n")
+        out.flush()
+        log(line[:300])
+
+    def gpu_run(f, cfg, reps=3):
+        M.integrate(f, cfg, ctx=ctx)
+        best, r = 1e30, None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = M.integrate(f, cfg, ctx=ctx)
+            best = min(best, time.perf_counter() - t0)
+        return r, 1e3 * best
+
+    def cpu_run(fid, params, d, mc, itmax, ita, tau, seed, lo, hi):
+        t0 = time.perf_counter()
+        o = O.integrate("ref", fid, params, d, 50, mc, itmax, ita, tau, 1.5, 1.5, seed, 0, lo, hi, workers=threads)
+        return o, 1e3 * (time.perf_counter() - t0)
+
+    def both(config, name, f, fid, params, d, mc, itmax, ita, tau, seed=1, lo=None, hi=None, cpu=True):
+        lo = lo or [0.0] * d
+        hi = hi or [1.0] * d
+        cfg = M.RunConfig(dims=d, maxcalls=mc, itmax=itmax, ita=ita, tau_rel=tau, seed=seed, lower=lo, upper=hi)
+        r, gms = gpu_run(f, cfg)
+        row = dict(config=config, integrand=name, dims=d, maxcalls=mc, itmax=itmax, ita=ita, tau_rel=tau, seed=seed,
+                   evals=r.total_samples, gpu_ms=gms, gpu_evals_per_s=r.total_samples / (gms * 1e-3),
+                   gpu_iterations=r.iterations_used, gpu_converged=r.converged, gpu_estimate=r.estimate,
+                   gpu_sigma=r.sigma, gpu_chi2_dof=r.chi2_dof, truth=f.reference)
+        if cpu:
+            o, cms = cpu_run(fid, params, d, mc, itmax, ita, tau, seed, lo, hi)
+            row.update(cpu_ms=cms, cpu_threads=threads, cpu_iterations=o["iterations_used"],
+                       cpu_converged=o["converged"], cpu_estimate=o["estimate"], cpu_sigma=o["sigma"],
+                       speedup=cms / gms, same_iterations=o["iterations_used"] == r.iterations_used,
+                       same_convergence=o["converged"] == r.converged,
+                       estimate_bitwise_equal=o["estimate"] == r.estimate,
+                       within_3_combined_sigma=abs(o["estimate"] - r.estimate) <= 3 * math.hypot(o["sigma"], r.sigma))
+        emit(row)
+
+    # C1: 5D f4, ncall 1e6, 10 iterations (the reference's CPU-runnable case)
+    both("C1", "f4", M.make_suite_integrand(4, 5), 4, None, 5, 10 ** 6, 10, 10, 1e-9, seed=0)
+    # C2: the 8D suite, time-to-epsrel at tau 1e-3 and 2e-4 (itmax 30, ita 10)
+    for fam in range(1, 7):
+        for tau in (1e-3, 2e-4):
+            both("C2", f"f{fam}", M.make_suite_integrand(fam, 8), fam, None, 8, 10 ** 7, 30, 10, tau)
+    for fam in (3, 5):  # GPU-only deeper tolerances at 1e9 evals/iteration
+        for tau in (4e-5, 8e-6, 1.6e-6):
+            both("C2", f"f{fam}", M.make_suite_integrand(fam, 8), fam, None, 8, 10 ** 9, 30, 10, tau, cpu=False)
+    # C3: 6D f4 at 1e9 evals/iteration (3 iterations on both sides)
+    both("C3", "f4", M.make_suite_integrand(4, 6), 4, None, 6, 10 ** 9, 3, 3, 1e-12)
+    # C4: 6D table integrand (device-resident interpolation tables, CPU twin on the host)
+    d, n = 6, 4096
+    t = np.linspace(0, 1, n)
+    rng = np.random.default_rng(0)
+    tabs = np.array([0.2 + np.exp(-0.5 * ((t - rng.uniform(0.3, 0.7)) / rng.uniform(0.05, 0.2)) ** 2)
+                     for _ in range(d)])
+    ft = M.make_table_integrand(tabs, [0.0] * d, [1.0] * d)
+    both("C4", "table6d", ft, 9, ft.params, d, 10 ** 8, 10, 10, 1e-12)
+    both("C4", "table6d", ft, 9, ft.params, d, 10 ** 10, 3, 3, 1e-12, cpu=False)
+    # C5: dims x ncall scaling (itmax 5, ita 3); CPU legs up to 1e8
+    for dd in (2, 4, 6, 8, 10):
+        for mc in (10 ** 6, 10 ** 8, 10 ** 10):
+            both("C5", "f4", M.make_suite_integrand(4, dd), 4, None, dd, mc, 5, 3, 1e-15, cpu=mc <= 10 ** 8)
+    out.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,6 +459,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--maxcalls", type=int, default=MAXCALLS)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
+    ap.add_argument("--suite", default=None, help="run BASELINE configs 1-5 (GPU + reference CPU) into this JSONL")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")
@@ -387,6 +470,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    if args.suite:
+        return run_suite(args.suite)
     if world > 1:
         import torch
         import torch.distributed as dist
