@@ -45,6 +45,15 @@ N_BINS = 50
 OPS_PER_EVAL = 10 * DIMS + (9 + 1 + DIMS) + (3 * DIMS + 21)  # = 143 for d = 8
 FP64_LANES_PER_SM = 64
 REF_SAMPLE_MAXCALLS = 10 ** 8  # bounded CPU sample (m = 9^8, p = 2: 86.1M evals)
+RNG_DESC = {
+    "philox": "philox (north-star Philox4x32-10 keyed by (seed, iteration), counter (cube, sample, axis block); "
+              "FMA transform; statistically equivalent to the reference, bitwise equal to its C twin)",
+    "compat": "compat (the reference's keyed SplitMix stream and arithmetic order; bitwise equal to the reference)",
+}
+DATA = {
+    "philox": "synthetic (counter-based Philox stream; no input data)",
+    "compat": "synthetic (keyed SplitMix stream of the reference; no input data)",
+}
 
 
 def log(*a):
@@ -182,7 +191,7 @@ def run_ours(args, rank, world, local_rank):
     f = M.make_suite_integrand(FAMILY, DIMS)
     total_its = args.warmup + args.steps
     cfg = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
-                      tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS)
+                      tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=args.rng)
     run = M.Run(f, cfg, ctx)
     sp = M.setup(cfg)
     m, p = sp.m, sp.p
@@ -248,7 +257,7 @@ def run_ours(args, rank, world, local_rank):
     host_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
     host_edges[:] = run.grid().raw_edges
     cfg2 = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
-                       tau_rel=1e-15, seed=1, lower=[0.0] * DIMS, upper=[1.0] * DIMS)
+                       tau_rel=1e-15, seed=1, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=args.rng)
     run2 = M.Run(f, cfg2, ctx)
     run2.set_exchange(xbuf.data_ptr())
     out_edges = np.zeros(DIMS * N_BINS)
@@ -296,11 +305,11 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (keyed SplitMix stream of the reference; no input data)",
+        "data": DATA[args.rng],
         "config": {"workload": "8D Genz f4 adjusting m-Cubes iteration", "integrand": "f4", "dims": DIMS,
                    "n_bins": N_BINS, "maxcalls": args.maxcalls, "m": m, "p": p, "evals_per_step": evals_per_step,
                    "parallelism": f"cube-range partition x{world} + exact all-reduce" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) between timed steps", "rng": "compat (reference SplitMix)",
+                   "l2": "flushed (256 MiB write) between timed steps", "rng": RNG_DESC[args.rng],
                    "reductions": "exact (superaccumulator)"},
         "clocks": clk,
         "gpu_launches": launches,
@@ -309,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
                 "path": "C ABI mcb_run_set_grid/sample/reduce/finish/grid (host grid in, host grid out)"},
         "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved_tflops / peak_tflops, "traffic": traffic,
-                     "kernel": "vsample_kernel<F4,8,compat>", "kernel_ms": 1e3 * k1_avg_s,
+                     "kernel": f"vsample_kernel<F4,8,{args.rng}>", "kernel_ms": 1e3 * k1_avg_s,
                      "ops_per_eval": OPS_PER_EVAL,
                      "peak_source": f"FP64 issue: {sms} SMs x {FP64_LANES_PER_SM} lanes x {sm_max:.0f} MHz "
                                     "(MEASURED_PEAKS.json has no FP64 figure; profiles/microbench_r01.txt "
@@ -318,6 +327,51 @@ def run_ours(args, rank, world, local_rank):
         "result": {"estimate": res.estimate, "sigma": res.sigma, "chi2_dof": res.chi2_dof,
                    "truth": f.reference},
     }
+
+    if args.rng == "philox" and not args.no_compat:
+        # the same step on the reference's own stream and arithmetic order
+        # (bitwise equal to the CPU reference): device-timed like `value`
+        cfg3 = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
+                           tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng="compat")
+        run3 = M.Run(f, cfg3, ctx)
+        run3.set_exchange(xbuf.data_ptr())
+
+        def step3(it, evs):
+            evs[0].record(stream)
+            run3.sample(it, n0, n1)
+            evs[1].record(stream)
+            run3.reduce(it)
+            if dist is not None:
+                dist.all_reduce(xbuf)
+            run3.finish(it)
+
+        evs3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.warmup + args.steps)]
+        st3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for it in range(1, args.warmup + 1):
+            step3(it, evs3[it - 1])
+            flush.zero_()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        for i in range(args.steps):
+            st3[i][0].record(stream)
+            step3(args.warmup + 1 + i, evs3[args.warmup + i])
+            st3[i][1].record(stream)
+            flush.zero_()
+        torch.cuda.synchronize()
+        c_total = sum(a.elapsed_time(b) for a, b in st3)
+        if dist is not None:
+            t = torch.tensor([c_total], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            c_total = float(t.item())
+        c_k1 = 1e-3 * statistics.mean(a.elapsed_time(b) for a, b in evs3[args.warmup:])
+        c_ach = OPS_PER_EVAL * k1_evals / c_k1 / 1e12
+        line["compat"] = {"value": evals_per_step * args.steps / (c_total * 1e-3), "unit": UNIT,
+                          "rng": RNG_DESC["compat"], "kernel_ms": 1e3 * c_k1, "roofline_achieved": c_ach,
+                          "roofline_frac": c_ach / peak_tflops, "result": {"estimate": run3.result().estimate}}
+        run3.close()
 
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline()
@@ -458,6 +512,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--maxcalls", type=int, default=MAXCALLS)
+    ap.add_argument("--rng", choices=["philox", "compat"], default="philox",
+                    help="philox = the north-star stream (headline); compat = the reference's stream, bit-exact")
+    ap.add_argument("--no-compat", action="store_true", help="skip the secondary compat-stream measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
     ap.add_argument("--suite", default=None, help="run BASELINE configs 1-5 (GPU + reference CPU) into this JSONL")
     args = ap.parse_args()

@@ -62,7 +62,8 @@ enum mcb_integrand_id {
   MCB_T_ZERO = 37        /* 0                                             */
 };
 
-enum mcb_bin_update { MCB_BIN_ALL_AXES = 0, MCB_BIN_AXIS0_ONLY = 1 }; /* sampler.hpp:51-54 */
+enum mcb_bin_update { MCB_BIN_ALL_AXES = 0, MCB_BIN_AXIS0_ONLY = 1, /* sampler.hpp:51-54 */
+                      MCB_BIN_NONE = 2 /* frozen iteration (mcb_v_sample_philox only) */ };
 enum mcb_variant { MCB_VARIANT_MCUBES = 0, MCB_VARIANT_MCUBES1D = 1 }; /* driver.hpp:23 */
 enum mcb_rng { MCB_RNG_COMPAT = 0, MCB_RNG_PHILOX = 1 };
 
@@ -149,8 +150,10 @@ int mcb_v_sample_no_adjust(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, 
                            uint64_t m, uint64_t s, uint64_t p, uint64_t seed, uint64_t iteration,
                            double* estimate, double* variance);
 
-/* ---- Philox-stream variant of v_sample (north-star RNG; not bitwise comparable
- * with the reference, statistically equivalent). ---- */
+/* ---- Philox-path variant of v_sample (north-star RNG + FMA-contracted
+ * transform; not bitwise comparable with the reference, statistically
+ * equivalent).  bin_update = MCB_BIN_NONE runs the frozen iteration
+ * (v_sample_no_adjust) and leaves contrib / writes untouched. ---- */
 int mcb_v_sample_philox(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,
                         const double* lower, const double* upper, const double* edges, uint64_t m,
                         uint64_t s, uint64_t p, uint64_t seed, uint64_t iteration,

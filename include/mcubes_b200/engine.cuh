@@ -179,6 +179,15 @@ struct Launch {
   std::size_t smem = 0;
 };
 
+/// Constants of the Philox path: z = u32 * cs + digit * nbg, J = nb^D * prod(width).
+inline void set_fast_constants(SampleArgs& a, const Shape& sh, int D) {
+  a.nbg = static_cast<double>(sh.nb) / static_cast<double>(sh.g);
+  a.cs = a.nbg * 0x1.0p-32;
+  double pw = 1.0;
+  for (int j = 0; j < D; ++j) pw *= static_cast<double>(sh.nb);
+  a.nbpow = pw;
+}
+
 template <class F, int D, RngKind R>
 Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes,
                  std::uint64_t iter_root, std::uint64_t n0, std::uint64_t n1, const int* stop,
@@ -216,6 +225,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.nbd = static_cast<double>(sh.nb);
   a.gd = static_cast<double>(sh.g);
   a.rcp_g = sh.rcp_g;
+  set_fast_constants(a, sh, D);
   a.scale = sh.scale;
   a.pp1 = sh.pp1;
   a.rcp_pp1 = sh.rcp_pp1;
@@ -254,6 +264,7 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
   a.nbd = static_cast<double>(sh.nb);
   a.gd = static_cast<double>(sh.g);
   a.rcp_g = sh.rcp_g;
+  set_fast_constants(a, sh, D);
   a.iter_root = iter_root;
   const std::size_t smem = 2 * sizeof(double) * D * sh.nb;
   auto kern = sample_point_kernel<F, D, R>;

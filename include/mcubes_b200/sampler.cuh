@@ -56,6 +56,9 @@ struct SampleArgs {
   double scale;    ///< 1.0 / (double(m) * double(p))   (sampler.hpp:293)
   double pp1;      ///< double(p) * double(p - 1)       (sampler.hpp:178)
   double rcp_pp1;  ///< RN(1/pp1)
+  double cs;       ///< philox: nb / (g * 2^32)   (32-bit uniform -> bin coordinate)
+  double nbg;      ///< philox: nb / g            (cube digit -> bin coordinate)
+  double nbpow;    ///< philox: nb^D              (jacobian = nb^D * prod widths)
   std::uint64_t iter_root;  ///< compat: iteration_root(seed, it); philox: the key
   std::uint64_t n0, n1;     ///< this launch's slice of the linear work index
   std::uint64_t A;          ///< cube(n) = n*A mod m
@@ -104,28 +107,68 @@ __device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
   }
 }
 
+/// Philox path: per-bin {A, width} with A = left - i*width, so the point is
+/// one FMA of the bin coordinate z: x = A + z*width (= left + (z-i)*width up
+/// to one rounding).
+template <int D>
+__device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a) {
+  const std::uint32_t nb = a.nb;
+  for (std::uint32_t idx = threadIdx.x; idx < D * nb; idx += blockDim.x) {
+    const std::uint32_t j = idx / nb, i = idx % nb;
+    const double* row = a.edges + static_cast<std::size_t>(j) * nb;
+    const double left = i == 0 ? a.lower[j] : row[i - 1];
+    const double w = __dsub_rn(row[i], left);
+    LW[idx] = make_double2(__fma_rn(-static_cast<double>(i), w, left), w);
+  }
+}
+
+/// Philox path, one sample: D uniforms from ceil(D/4) Philox4x32-10 blocks
+/// keyed by the iteration with counter (cube, sample, block); bin coordinate
+/// z = (digit + u) * nb / g as one FMA from the per-cube base; point and
+/// jacobian from the {A, width} table.  Returns f*J.
+template <class F, int D>
+__device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, const double2* LW,
+                                                    const double (&base)[D], std::uint64_t t, std::uint32_t k,
+                                                    double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
+  const std::uint32_t nb = a.nb, nbm1 = nb - 1;
+  const std::uint32_t k0 = static_cast<std::uint32_t>(a.iter_root), k1 = static_cast<std::uint32_t>(a.iter_root >> 32);
+  std::uint32_t r[(D + 3) & ~3];
+#pragma unroll
+  for (int q = 0; q < (D + 3) / 4; ++q) {
+    const rng::U4 o = rng::philox4x32_10(
+        rng::U4{static_cast<std::uint32_t>(t), static_cast<std::uint32_t>(t >> 32), k, static_cast<std::uint32_t>(q)}, k0,
+        k1);
+    r[4 * q] = o.x;
+    r[4 * q + 1] = o.y;
+    r[4 * q + 2] = o.z;
+    r[4 * q + 3] = o.w;
+  }
+  double jw = 1.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double z = __fma_rn(__uint2double_rn(r[j]), a.cs, base[j]);
+    std::uint32_t i = __double2uint_rz(z);
+    i = i < nbm1 ? i : nbm1;
+    const double2 lw = LW[j * nb + i];
+    x[j] = __fma_rn(z, lw.y, lw.x);
+    jw = j == 0 ? lw.y : __dmul_rn(jw, lw.y);
+    bin[j] = i;
+  }
+  fx = static_cast<double>(f(std::span<const double>(x, D)));
+  return __dmul_rn(fx, __dmul_rn(jw, a.nbpow));
+}
+
 /// One sample: point, jacobian, bins and f*J of sample k of a cube
 /// (sampler.hpp:163-170 with transform_impl, grid.hpp:204-224).
-template <class F, int D, RngKind R>
+template <class F, int D>
 __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double2* LW,
-                                               const double (&dg)[D], std::uint64_t t,
-                                               std::uint64_t croot, std::uint32_t k, double (&x)[D],
-                                               std::uint32_t (&bin)[D], double& fx) {
+                                               const double (&dg)[D], std::uint64_t croot, std::uint32_t k,
+                                               double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
   const std::uint32_t nb = a.nb, nbm1 = nb - 1;
   double r[D];
-  if constexpr (R == RngKind::compat) {
-    const std::uint64_t proot = rng::feed(croot, k);  // rng.hpp:55-58
+  const std::uint64_t proot = rng::feed(croot, k);  // rng.hpp:55-58
 #pragma unroll
-    for (int j = 0; j < D; ++j) r[j] = rng::to_unit(rng::feed(proot, static_cast<std::uint64_t>(j)));
-  } else {
-#pragma unroll
-    for (int j = 0; j < D; j += 2) {
-      double r0, r1;
-      rng::philox_pair(a.iter_root, t, k, static_cast<std::uint32_t>(j >> 1), r0, r1);
-      r[j] = r0;
-      if (j + 1 < D) r[j + 1] = r1;
-    }
-  }
+  for (int j = 0; j < D; ++j) r[j] = rng::to_unit(rng::feed(proot, static_cast<std::uint64_t>(j)));
   double jac = 1.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -158,7 +201,8 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   {  // zero the accumulators, stage the grid and the Welford reciprocals
     const int nwords = nacc * kXWords;
     for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
-    stage_grid<D>(LW, a);
+    if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
+    else stage_grid_fast<D>(LW, a);
     for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
   }
   __syncthreads();
@@ -169,6 +213,25 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   std::uint32_t* var_acc = acc + (2 * kLaneCopies + lane) * kXWords;
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
   std::uint32_t* const acc_end = acc + nacc * kXWords;
+  const std::uint32_t bin_axes = a.bin_axes;
+
+  // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once,
+  // deposit word-major across the axes
+  auto deposit = [&](double fj, const std::uint32_t (&bin)[D]) {
+    exact::Digits dgt;
+    if (exact::split(__dmul_rn(fj, fj), dgt)) {
+      std::uint32_t* const base = bins + dgt.w;
+      if (bin_axes == static_cast<std::uint32_t>(D)) {
+        std::uint32_t* ptrs[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) ptrs[j] = base + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords;
+        exact::add_digits_n<D>(ptrs, acc_end, dgt);
+      } else {  // BinUpdate::axis0_only
+        std::uint32_t* const ptrs[1] = {base + bin[0] * kXWords};
+        exact::add_digits_n<1>(ptrs, acc_end, dgt);
+      }
+    }
+  };
 
   const std::uint64_t T = static_cast<std::uint64_t>(gridDim.x) * nt;
   std::uint64_t n = a.n0 + static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
@@ -186,48 +249,63 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
         tt /= a.g;
       }
     }
-    const std::uint32_t bin_axes = a.bin_axes;
     const std::uint32_t p = static_cast<std::uint32_t>(a.p);
     for (; n < a.n1; n += T) {
-      double dg[D];
+      double sum, var;
+      if constexpr (R == RngKind::compat) {
+        double dg[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) dg[j] = static_cast<double>(dig[j]);
-      const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
-      double sum = 0.0, mean = 0.0, m2 = 0.0;
-      for (std::uint32_t k = 0; k < p; ++k) {
-        double x[D];
-        std::uint32_t bin[D];
-        double fx;
-        const double fj = sample_point<F, D, R>(a, f, LW, dg, t, croot, k, x, bin, fx);
-        if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
-          atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-          continue;
-        }
-        sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
-        // Welford (sampler.hpp:98-103)
-        const std::uint32_t nk = k + 1;
-        const double dd = __dsub_rn(fj, mean);
-        const double q = nk < static_cast<std::uint32_t>(kRcpSmem) ? div_rn(dd, static_cast<double>(nk), rcp[nk])
-                                                                   : __ddiv_rn(dd, static_cast<double>(nk));
-        mean = __dadd_rn(mean, q);
-        m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
-        if (bin_axes) {  // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once
-          exact::Digits dgt;
-          if (exact::split(__dmul_rn(fj, fj), dgt)) {
-            std::uint32_t* const base = bins + dgt.w;
-            if (bin_axes == static_cast<std::uint32_t>(D)) {
-              std::uint32_t* ptrs[D];
-#pragma unroll
-              for (int j = 0; j < D; ++j) ptrs[j] = base + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords;
-              exact::add_digits_n<D>(ptrs, acc_end, dgt);
-            } else {  // BinUpdate::axis0_only
-              std::uint32_t* const ptrs[1] = {base + bin[0] * kXWords};
-              exact::add_digits_n<1>(ptrs, acc_end, dgt);
-            }
+        for (int j = 0; j < D; ++j) dg[j] = static_cast<double>(dig[j]);
+        const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
+        double mean = 0.0, m2 = 0.0;
+        sum = 0.0;
+        for (std::uint32_t k = 0; k < p; ++k) {
+          double x[D];
+          std::uint32_t bin[D];
+          double fx;
+          const double fj = sample_point<F, D>(a, f, LW, dg, croot, k, x, bin, fx);
+          if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
+            atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+            continue;
           }
+          sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
+          // Welford (sampler.hpp:98-103)
+          const std::uint32_t nk = k + 1;
+          const double dd = __dsub_rn(fj, mean);
+          const double q = nk < static_cast<std::uint32_t>(kRcpSmem) ? div_rn(dd, static_cast<double>(nk), rcp[nk])
+                                                                     : __ddiv_rn(dd, static_cast<double>(nk));
+          mean = __dadd_rn(mean, q);
+          m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
+          if (bin_axes) deposit(fj, bin);
         }
+        var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
+      } else {
+        // Philox path: same estimator (sum of f*J, Welford variance of the
+        // mean), FMA-contracted arithmetic; validated statistically.
+        double base[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) base[j] = __dmul_rn(static_cast<double>(dig[j]), a.nbg);
+        double mean = 0.0, m2 = 0.0;
+        sum = 0.0;
+        for (std::uint32_t k = 0; k < p; ++k) {
+          double x[D];
+          std::uint32_t bin[D];
+          double fx;
+          const double fj = sample_point_fast<F, D>(a, f, LW, base, t, k, x, bin, fx);
+          if (!isfinite(fj)) {
+            atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+            continue;
+          }
+          sum = __dadd_rn(sum, fj);
+          const double dd = __dsub_rn(fj, mean);
+          mean = __fma_rn(dd, rcp[k + 1 < static_cast<std::uint32_t>(kRcpSmem) ? k + 1 : 0], mean);
+          if (k + 1 >= static_cast<std::uint32_t>(kRcpSmem)) mean = __dadd_rn(mean, __ddiv_rn(dd, static_cast<double>(k + 1)));
+          m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
+          if (bin_axes) deposit(fj, bin);
+        }
+        sum = __dmul_rn(sum, a.scale);
+        var = __dmul_rn(m2, a.rcp_pp1);
       }
-      double var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
       if (!(var > 0.0)) var = 0.0;
       std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
       exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
@@ -272,7 +350,8 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
                                     double* out_x, double* out_fx) {
   extern __shared__ __align__(16) unsigned char smem[];
   double2* LW = reinterpret_cast<double2*>(smem);
-  stage_grid<D>(LW, a);
+  if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
+  else stage_grid_fast<D>(LW, a);
   __syncthreads();
   if (threadIdx.x != 0) return;
   double dg[D];
@@ -284,7 +363,13 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
   double x[D];
   std::uint32_t bin[D];
   double fx;
-  sample_point<F, D, R>(a, f, LW, dg, t, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
+  if constexpr (R == RngKind::compat) {
+    sample_point<F, D>(a, f, LW, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
+  } else {
+    double base[D];
+    for (int j = 0; j < D; ++j) base[j] = __dmul_rn(dg[j], a.nbg);
+    sample_point_fast<F, D>(a, f, LW, base, t, static_cast<std::uint32_t>(k), x, bin, fx);
+  }
   for (int j = 0; j < D; ++j) out_x[j] = x[j];
   *out_fx = fx;
 }

@@ -71,6 +71,8 @@ def orc():
         lib.orc_check_convergence.argtypes = [_D, _D, _D, _D, _D]
         lib.orc_integrate.argtypes = [_I, _PD, _U32, _U32, _U32, _U64, _U32, _U32, _D, _D, _D, _U64,
                                       _I, _PD, _PD, _PD, _PU64, _PD, _PD, _U32, _PD, _PU64, _PD, _PD]
+        lib.orc_set_rng.argtypes = [_I]
+        lib.orc_set_rng.restype = None
         lib.orc_xwords.restype = _U32
         assert lib.orc_xwords() == XWORDS
         _orc = lib
@@ -143,10 +145,12 @@ class OracleError(RuntimeError):
 
 
 def v_sample(lib_kind, integrand, params, d, nb, lower, upper, edges, m, s, p, seed, iteration,
-             mode="all", threads=0):
+             mode="all", threads=0, rng="compat"):
     """Run one iteration through the oracle ('orc') or compiled reference ('ref').
 
     mode: 'all' | 'axis0' | 'frozen' | 'serial' (ref only: vegas_serial_iteration).
+    rng: 'compat' (the reference stream) or 'philox' (orc only: the C twin of
+    the B200 Philox path, which the reference does not have).
     Returns dict(est, var, contrib(np, d*nb) or None, writes).
     """
     np = _np()
@@ -172,9 +176,13 @@ def v_sample(lib_kind, integrand, params, d, nb, lower, upper, edges, m, s, p, s
             ep = ptr(e)
         bin_mode = 1 if mode in ("axis0", "serial_axis0") else 0
         kbins = 0 if mode == "frozen" else 1
-        rc = lib.orc_v_sample(integrand, ptr(params), len(params), d, nb, lo, hi, ep, m, s, p, seed,
-                              iteration, bin_mode, kbins, C.byref(est), C.byref(var), ptr(contrib),
-                              C.byref(writes), ptr(ex), C.byref(efx))
+        lib.orc_set_rng(1 if rng == "philox" else 0)
+        try:
+            rc = lib.orc_v_sample(integrand, ptr(params), len(params), d, nb, lo, hi, ep, m, s, p, seed,
+                                  iteration, bin_mode, kbins, C.byref(est), C.byref(var), ptr(contrib),
+                                  C.byref(writes), ptr(ex), C.byref(efx))
+        finally:
+            lib.orc_set_rng(0)
         err = lib.orc_last_error
     if rc != 0:
         raise OracleError(rc, err().decode(), ex[:d].copy(), efx.value)
@@ -183,7 +191,7 @@ def v_sample(lib_kind, integrand, params, d, nb, lower, upper, edges, m, s, p, s
 
 
 def integrate(lib_kind, integrand, params, d, nb, maxcalls, itmax, ita, tau, alpha, chi2max, seed,
-              variant, lower, upper, workers=0, want_grids=False):
+              variant, lower, upper, workers=0, want_grids=False, rng="compat"):
     np = _np()
     params = np.ascontiguousarray(params if params is not None else [], dtype=np.float64)
     res = np.zeros(8)
@@ -203,9 +211,13 @@ def integrate(lib_kind, integrand, params, d, nb, maxcalls, itmax, ita, tau, alp
         err = lib.ref_last_error
     else:
         lib = orc()
-        rc = lib.orc_integrate(integrand, ptr(params), len(params), d, nb, maxcalls, itmax, ita, tau,
-                               alpha, chi2max, seed, variant, darr(lower), darr(upper), ptr(res), sp,
-                               ptr(he), ptr(hv), itmax, ptr(grids), wr, ptr(ex), C.byref(efx))
+        lib.orc_set_rng(1 if rng == "philox" else 0)
+        try:
+            rc = lib.orc_integrate(integrand, ptr(params), len(params), d, nb, maxcalls, itmax, ita, tau,
+                                   alpha, chi2max, seed, variant, darr(lower), darr(upper), ptr(res), sp,
+                                   ptr(he), ptr(hv), itmax, ptr(grids), wr, ptr(ex), C.byref(efx))
+        finally:
+            lib.orc_set_rng(0)
         err = lib.orc_last_error
     if rc != 0:
         raise OracleError(rc, err().decode(), ex.copy(), efx.value)

@@ -442,6 +442,89 @@ static void run_cube(const orc_fn* f, const orc_grid* g, uint64_t t, uint64_t gi
   xacc_add_mag(&acc->var, var);
 }
 
+/* ---------------- Philox path twin (NOT the reference) ----------------
+ * The B200 north-star stream (include/mcubes_b200/sampler.cuh,
+ * sample_point_fast): Philox4x32-10 keyed by the iteration root with counter
+ * (cube lo, cube hi, sample, block of 4 axes), 32-bit uniforms, FMA-contracted
+ * transform and Welford.  The reference has no such mode; this restatement
+ * lets tests check the GPU Philox path bit for bit on integrands built from + - * and /, while
+ * its agreement with the reference itself is statistical (3 combined sigma). */
+static void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint64_t gi, uint64_t p,
+                            uint64_t key, double scale, uint32_t bin_axes, int kbins, partial* acc) {
+  const uint32_t d = g->d, nb = g->nb;
+  const double nbg = (double)nb / (double)gi, cs = nbg * 0x1.0p-32;
+  double nbpow = 1.0;
+  for (uint32_t j = 0; j < d; ++j) nbpow *= (double)nb;
+  double base[64], x[64];
+  uint32_t bin[64], r[68];
+  uint64_t tt = t;
+  for (uint32_t j = 0; j < d; ++j) {
+    base[j] = (double)(tt % gi) * nbg;
+    tt /= gi;
+  }
+  double sum = 0.0, mean = 0.0, m2 = 0.0;
+  for (uint64_t k = 0; k < p; ++k) {
+    for (uint32_t q = 0; q < (d + 3) / 4; ++q) {
+      uint32_t c[4] = {(uint32_t)t, (uint32_t)(t >> 32), (uint32_t)k, q};
+      philox4x32_10(c, (uint32_t)key, (uint32_t)(key >> 32));
+      memcpy(r + 4 * q, c, sizeof c);
+    }
+    double jw = 1.0;
+    for (uint32_t j = 0; j < d; ++j) {
+      const double z = fma((double)r[j], cs, base[j]);
+      uint32_t i = (uint32_t)z;
+      if (i > nb - 1) i = nb - 1;
+      const double* row = g->edges + (size_t)j * nb;
+      const double left = i == 0 ? g->lower[j] : row[i - 1];
+      const double w = row[i] - left;
+      const double A = fma(-(double)i, w, left);
+      x[j] = fma(z, w, A);
+      jw = j == 0 ? w : jw * w;
+      bin[j] = i;
+    }
+    const double fx = eval_fn(f, x);
+    const double fj = fx * (jw * nbpow);
+    if (!isfinite(fj)) {
+      if (!acc->bad) {
+        acc->bad = 1;
+        acc->bad_fx = fx;
+        memcpy(acc->bad_x, x, sizeof(double) * d);
+      }
+      return;
+    }
+    sum += fj;
+    const double dd = fj - mean;
+    const uint64_t nk = k + 1;
+    mean = fma(dd, nk < 64 ? 1.0 / (double)nk : 0.0, mean);
+    if (nk >= 64) mean = mean + dd / (double)nk;
+    m2 = fma(dd, fj - mean, m2);
+    if (kbins) {
+      const double sq = fj * fj;
+      for (uint32_t j = 0; j < bin_axes; ++j) xacc_add_mag(&acc->bins[(size_t)j * nb + bin[j]], sq);
+      acc->writes += bin_axes;
+    }
+  }
+  sum = sum * scale;
+  double var = m2 * (1.0 / ((double)p * (double)(p - 1)));
+  if (!(var > 0.0)) var = 0.0;
+  xacc_add_mag(sum < 0 ? &acc->est_neg : &acc->est_pos, sum);
+  xacc_add_mag(&acc->var, var);
+}
+
+static int g_rng = 0; /* 0 = the reference stream, 1 = the Philox path twin */
+void orc_set_rng(int rng) { g_rng = rng; }
+
 /* Exact partial over cubes [c0, c1) in the GPU exchange format: out_words
  * receives (3 + bin_axes*nb) accumulators of XW words:
  * [est_pos, est_neg, var, bins...].  This is what one rank contributes before
@@ -467,7 +550,8 @@ int orc_sample_partial(int id, const double* params, uint32_t nparams, uint32_t 
   acc.bins = calloc((size_t)bin_axes * nb, sizeof(xacc));
   const uint64_t iter_root = orc_iteration_root(seed, iteration);
   for (uint64_t t = c0; t < c1 && t < m; ++t) {
-    run_cube(&f, &g, t, gi, p, iter_root, scale, bin_axes, kbins, &acc);
+    if (g_rng) run_cube_philox(&f, &g, t, gi, p, iter_root, scale, bin_axes, kbins, &acc);
+    else run_cube(&f, &g, t, gi, p, iter_root, scale, bin_axes, kbins, &acc);
     if (acc.bad) break;
   }
   if (acc.bad) {

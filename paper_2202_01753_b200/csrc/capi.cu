@@ -219,9 +219,10 @@ int mcb_v_sample_philox(mcb_ctx* c, const mcb_integrand* f, uint32_t dims, uint3
                         const double* upper, const double* edges, uint64_t m, uint64_t s, uint64_t p,
                         uint64_t seed, uint64_t iteration, int32_t bin_update, double* est, double* var,
                         double* contrib, uint64_t* writes) {
-  return v_sample_impl(c, f, dims, n_bins, lower, upper, edges, m, s, p, seed, iteration,
-                       bin_update == MCB_BIN_AXIS0_ONLY ? MCB_BIN_AXIS0_ONLY : MCB_BIN_ALL_AXES, RngKind::philox,
-                       est, var, contrib, writes);
+  const int32_t mode = bin_update == MCB_BIN_NONE ? -1
+                       : bin_update == MCB_BIN_AXIS0_ONLY ? MCB_BIN_AXIS0_ONLY : MCB_BIN_ALL_AXES;
+  return v_sample_impl(c, f, dims, n_bins, lower, upper, edges, m, s, p, seed, iteration, mode, RngKind::philox,
+                       est, var, mode < 0 ? nullptr : contrib, mode < 0 ? nullptr : writes);
 }
 
 int mcb_v_sample_no_adjust(mcb_ctx* c, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,

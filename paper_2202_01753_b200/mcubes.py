@@ -535,14 +535,20 @@ def v_sample(f: IntegrandSpec, grid: Grid, m: int, s: int, p: int, seed: int, it
 
 
 def v_sample_no_adjust(f: IntegrandSpec, grid: Grid, m: int, s: int, p: int, seed: int, iteration: int,
-                       max_threads: int = 0, ctx: Optional[Context] = None) -> EstimateVariance:
+                       max_threads: int = 0, rng: str = "compat", ctx: Optional[Context] = None) -> EstimateVariance:
     """Frozen-grid iteration on the GPU (sampler.hpp:339-349)."""
     ctx = ctx or default_context()
     fs, keep = f._c()
     lo, hi = _f64(grid.lowers), _f64(grid.uppers)
     est, var = C.c_double(), C.c_double()
-    rc = L.lib().mcb_v_sample_no_adjust(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo), _dptr(hi),
-                                        _dptr(grid.raw_edges), m, s, p, seed, iteration, C.byref(est), C.byref(var))
+    if rng == "philox":
+        rc = L.lib().mcb_v_sample_philox(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo), _dptr(hi),
+                                         _dptr(grid.raw_edges), m, s, p, seed, iteration, 2, C.byref(est),
+                                         C.byref(var), None, None)
+    else:
+        rc = L.lib().mcb_v_sample_no_adjust(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo),
+                                            _dptr(hi), _dptr(grid.raw_edges), m, s, p, seed, iteration,
+                                            C.byref(est), C.byref(var))
     _raise(rc, ctx.ptr, grid.dims())
     return EstimateVariance(est.value, var.value)
 
