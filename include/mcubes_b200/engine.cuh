@@ -179,6 +179,17 @@ struct Launch {
   std::size_t smem = 0;
 };
 
+/// Philox4x32-10 key schedule of the iteration key (uniform per launch).
+inline void set_round_keys(SampleArgs& a, std::uint64_t key) {
+  std::uint32_t k0 = static_cast<std::uint32_t>(key), k1 = static_cast<std::uint32_t>(key >> 32);
+  for (int r = 0; r < 10; ++r) {
+    a.round_keys[2 * r] = k0;
+    a.round_keys[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
 /// Constants of the Philox path: z = u32 * cs + digit * nbg, J = nb^D * prod(width).
 inline void set_fast_constants(SampleArgs& a, const Shape& sh, int D) {
   a.nbg = static_cast<double>(sh.nb) / static_cast<double>(sh.g);
@@ -188,11 +199,11 @@ inline void set_fast_constants(SampleArgs& a, const Shape& sh, int D) {
   a.nbpow = pw;
 }
 
-template <class F, int D, RngKind R>
+template <class F, int D, RngKind R, int NB = 0>
 Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes,
                  std::uint64_t iter_root, std::uint64_t n0, std::uint64_t n1, const int* stop,
                  unsigned long long* err_key) {
-  auto kern = vsample_kernel<F, D, R>;
+  auto kern = vsample_kernel<F, D, R, NB>;
   Launch L;
   L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
   if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
@@ -230,6 +241,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.pp1 = sh.pp1;
   a.rcp_pp1 = sh.rcp_pp1;
   a.iter_root = iter_root;
+  set_round_keys(a, iter_root);
   a.n0 = n0;
   a.n1 = n1;
   a.A = sh.A;
@@ -266,6 +278,7 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
   a.rcp_g = sh.rcp_g;
   set_fast_constants(a, sh, D);
   a.iter_root = iter_root;
+  set_round_keys(a, iter_root);
   const std::size_t smem = 2 * sizeof(double) * D * sh.nb;
   auto kern = sample_point_kernel<F, D, R>;
   MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -286,7 +299,10 @@ Launch dispatch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_
   switch (sh.dims) {
 #define MCB_CASE(D) \
   case D:           \
-    if constexpr (D <= MCB_DIMS_MAX) return launch_k1<F, D, R>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key); \
+    if constexpr (D <= MCB_DIMS_MAX) {                                                                                  \
+      if (sh.nb == 50) return launch_k1<F, D, R, 50>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key);          \
+      return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key);                            \
+    }                                                                                                                   \
     break;
     MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
     MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16)

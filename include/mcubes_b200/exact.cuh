@@ -124,6 +124,51 @@ __device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::
   }
 }
 
+// ---- the same deposits on 32-bit shared-window addresses (atom.shared):
+// no 64-bit generic-pointer arithmetic per axis, and constant per-axis row
+// offsets fold into the instruction's immediate.
+__device__ __forceinline__ std::uint32_t atoms_add(std::uint32_t addr, std::uint32_t v) {
+  std::uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+
+template <int kTag = 0>
+__device__ __noinline__ void carry_up_s(std::uint32_t addr, std::uint32_t end) {
+  for (; addr < end; addr += 4)
+    if (atoms_add(addr, 1u) != 0xffffffffu) break;
+}
+
+/// add_digits_n on shared-window byte addresses a[j] (= accumulator j + 4 dg.w).
+template <int N>
+__device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::uint32_t end, const Digits& dg) {
+  std::uint32_t t1[N], u[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t o = atoms_add(a[j], dg.d0);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
+        : "=r"(t1[j]), "=r"(u[j])
+        : "r"(o), "r"(dg.d0), "r"(dg.d1), "r"(dg.d2));
+  }
+  std::uint32_t t2[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t o = atoms_add(a[j] + 4, t1[j]);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(t2[j]) : "r"(o), "r"(t1[j]), "r"(u[j]));
+  }
+  std::uint32_t ripple = 0;  // bit (N-1-j) = carry out of axis j's top word
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t o = atoms_add(a[j] + 8, t2[j]);
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t2[j]));
+  }
+  if (ripple) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(a[j] + 12, end);
+  }
+}
+
 /// Two independent exact adds (the per-cube estimate and variance), issued
 /// interleaved so their atomic round trips overlap.
 __device__ __forceinline__ void add_shared2(std::uint32_t* acc_a, double a, std::uint32_t* acc_b, double b,

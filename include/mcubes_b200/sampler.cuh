@@ -64,6 +64,7 @@ struct SampleArgs {
   std::uint64_t A;          ///< cube(n) = n*A mod m
   std::uint64_t stepT;      ///< (gridDim*blockDim*A) mod m
   std::uint64_t step_digits[kMaxDims];  ///< base-g digits of stepT (axis 0 first)
+  std::uint32_t round_keys[20];         ///< philox: (k0, k1) of rounds 0..9 (uniform; folded into LOP3)
   std::uint32_t* partials;             ///< bins: [gridDim][kXWords][bin_axes*nb] u32
   unsigned long long* scal_partials;   ///< est+/est-/var: [gridDim][3][kXWords] u64 (lane copies folded)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
@@ -122,22 +123,34 @@ __device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a
   }
 }
 
+/// Philox4x32-10 with the per-round keys read from the launch parameters
+/// (constant bank), so a round is two IMAD.WIDE + two LOP3.
+__device__ __forceinline__ rng::U4 philox_rk(rng::U4 c, const std::uint32_t (&rk)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const std::uint64_t p0 = static_cast<std::uint64_t>(0xD2511F53u) * c.x;
+    const std::uint64_t p1 = static_cast<std::uint64_t>(0xCD9E8D57u) * c.z;
+    c = rng::U4{static_cast<std::uint32_t>(p1 >> 32) ^ c.y ^ rk[2 * r], static_cast<std::uint32_t>(p1),
+                static_cast<std::uint32_t>(p0 >> 32) ^ c.w ^ rk[2 * r + 1], static_cast<std::uint32_t>(p0)};
+  }
+  return c;
+}
+
 /// Philox path, one sample: D uniforms from ceil(D/4) Philox4x32-10 blocks
 /// keyed by the iteration with counter (cube, sample, block); bin coordinate
 /// z = (digit + u) * nb / g as one FMA from the per-cube base; point and
 /// jacobian from the {A, width} table.  Returns f*J.
-template <class F, int D>
+template <class F, int D, int NB>
 __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, const double2* LW,
                                                     const double (&base)[D], std::uint64_t t, std::uint32_t k,
                                                     double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
-  const std::uint32_t nb = a.nb, nbm1 = nb - 1;
-  const std::uint32_t k0 = static_cast<std::uint32_t>(a.iter_root), k1 = static_cast<std::uint32_t>(a.iter_root >> 32);
+  const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb, nbm1 = nb - 1;
   std::uint32_t r[(D + 3) & ~3];
 #pragma unroll
   for (int q = 0; q < (D + 3) / 4; ++q) {
-    const rng::U4 o = rng::philox4x32_10(
-        rng::U4{static_cast<std::uint32_t>(t), static_cast<std::uint32_t>(t >> 32), k, static_cast<std::uint32_t>(q)}, k0,
-        k1);
+    const rng::U4 o = philox_rk(
+        rng::U4{static_cast<std::uint32_t>(t), static_cast<std::uint32_t>(t >> 32), k, static_cast<std::uint32_t>(q)},
+        a.round_keys);
     r[4 * q] = o.x;
     r[4 * q + 1] = o.y;
     r[4 * q + 2] = o.z;
@@ -160,11 +173,11 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
 
 /// One sample: point, jacobian, bins and f*J of sample k of a cube
 /// (sampler.hpp:163-170 with transform_impl, grid.hpp:204-224).
-template <class F, int D>
+template <class F, int D, int NB>
 __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double2* LW,
                                                const double (&dg)[D], std::uint64_t croot, std::uint32_t k,
                                                double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
-  const std::uint32_t nb = a.nb, nbm1 = nb - 1;
+  const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb, nbm1 = nb - 1;
   double r[D];
   const std::uint64_t proot = rng::feed(croot, k);  // rng.hpp:55-58
 #pragma unroll
@@ -187,11 +200,13 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
   return __dmul_rn(fx, jac);
 }
 
-template <class F, int D, RngKind R>
+/// K1.  NB = n_bins when known at compile time (50, the reference default
+/// and every BASELINE config), 0 = runtime n_bins.
+template <class F, int D, RngKind R, int NB = 0>
 __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const SampleArgs a, const F f) {
   if (a.stop && *a.stop) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  const std::uint32_t nb = a.nb;
+  const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb;
   double2* LW = reinterpret_cast<double2*>(smem);
   double* rcp = reinterpret_cast<double*>(LW + D * nb);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
@@ -213,22 +228,26 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
   std::uint32_t* var_acc = acc + (2 * kLaneCopies + lane) * kXWords;
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
   std::uint32_t* const acc_end = acc + nacc * kXWords;
+  // 32-bit shared-window byte addresses of the bin accumulators
+  const std::uint32_t bins_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(bins));
+  const std::uint32_t end_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(acc_end));
   const std::uint32_t bin_axes = a.bin_axes;
+  constexpr std::uint32_t kCell = 4u * kXWords;  // bytes per accumulator
 
   // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once,
   // deposit word-major across the axes
   auto deposit = [&](double fj, const std::uint32_t (&bin)[D]) {
     exact::Digits dgt;
     if (exact::split(__dmul_rn(fj, fj), dgt)) {
-      std::uint32_t* const base = bins + dgt.w;
+      const std::uint32_t wb = bins_s + 4u * dgt.w;
       if (bin_axes == static_cast<std::uint32_t>(D)) {
-        std::uint32_t* ptrs[D];
+        std::uint32_t ad[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) ptrs[j] = base + (static_cast<std::uint32_t>(j) * nb + bin[j]) * kXWords;
-        exact::add_digits_n<D>(ptrs, acc_end, dgt);
+        for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
+        exact::add_digits_s<D>(ad, end_s, dgt);
       } else {  // BinUpdate::axis0_only
-        std::uint32_t* const ptrs[1] = {base + bin[0] * kXWords};
-        exact::add_digits_n<1>(ptrs, acc_end, dgt);
+        const std::uint32_t ad[1] = {wb + bin[0] * kCell};
+        exact::add_digits_s<1>(ad, end_s, dgt);
       }
     }
   };
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
           double x[D];
           std::uint32_t bin[D];
           double fx;
-          const double fj = sample_point<F, D>(a, f, LW, dg, croot, k, x, bin, fx);
+          const double fj = sample_point<F, D, NB>(a, f, LW, dg, croot, k, x, bin, fx);
           if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
             atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
             continue;
@@ -291,15 +310,17 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
           double x[D];
           std::uint32_t bin[D];
           double fx;
-          const double fj = sample_point_fast<F, D>(a, f, LW, base, t, k, x, bin, fx);
+          const double fj = sample_point_fast<F, D, NB>(a, f, LW, base, t, k, x, bin, fx);
           if (!isfinite(fj)) {
             atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
             continue;
           }
           sum = __dadd_rn(sum, fj);
+          // Welford with y = RN(1/n): mean += (f - mean) * y
+          const std::uint32_t nk = k + 1;
+          const double y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
           const double dd = __dsub_rn(fj, mean);
-          mean = __fma_rn(dd, rcp[k + 1 < static_cast<std::uint32_t>(kRcpSmem) ? k + 1 : 0], mean);
-          if (k + 1 >= static_cast<std::uint32_t>(kRcpSmem)) mean = __dadd_rn(mean, __ddiv_rn(dd, static_cast<double>(k + 1)));
+          mean = __fma_rn(dd, y, mean);
           m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
           if (bin_axes) deposit(fj, bin);
         }
@@ -313,12 +334,25 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
       // advance to cube (n + T)*A mod m: odometer add of stepT's digits
       t += a.stepT;
       if (t >= a.m) t -= a.m;
-      Dig carry = 0;
+      if constexpr (sizeof(Dig) == 4) {
+        // v = dig + step + carry (< 2g < 2^31); w = v - g; digit = min(v, w)
+        // unsigned; carry = w >= 0, folded into the next axis' add
+        std::uint32_t borrow = 1;  // 1 - carry
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
-        carry = v >= g ? 1 : 0;
-        dig[j] = carry ? v - g : v;
+        for (int j = 0; j < D; ++j) {
+          const std::uint32_t v = dig[j] + static_cast<std::uint32_t>(a.step_digits[j]) + 1u - borrow;
+          const std::uint32_t w = v - g;
+          dig[j] = v < w ? v : w;
+          borrow = w >> 31;
+        }
+      } else {
+        Dig carry = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
+          carry = v >= g ? 1 : 0;
+          dig[j] = carry ? v - g : v;
+        }
       }
     }
   }
@@ -364,11 +398,11 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
   std::uint32_t bin[D];
   double fx;
   if constexpr (R == RngKind::compat) {
-    sample_point<F, D>(a, f, LW, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
+    sample_point<F, D, 0>(a, f, LW, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
   } else {
     double base[D];
     for (int j = 0; j < D; ++j) base[j] = __dmul_rn(dg[j], a.nbg);
-    sample_point_fast<F, D>(a, f, LW, base, t, static_cast<std::uint32_t>(k), x, bin, fx);
+    sample_point_fast<F, D, 0>(a, f, LW, base, t, static_cast<std::uint32_t>(k), x, bin, fx);
   }
   for (int j = 0; j < D; ++j) out_x[j] = x[j];
   *out_fx = fx;

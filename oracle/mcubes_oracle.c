@@ -506,8 +506,7 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
     sum += fj;
     const double dd = fj - mean;
     const uint64_t nk = k + 1;
-    mean = fma(dd, nk < 64 ? 1.0 / (double)nk : 0.0, mean);
-    if (nk >= 64) mean = mean + dd / (double)nk;
+    mean = fma(dd, 1.0 / (double)nk, mean);
     m2 = fma(dd, fj - mean, m2);
     if (kbins) {
       const double sq = fj * fj;

@@ -34,13 +34,13 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e1);
   const gpu::fn::F4 f{};
   gpu::Launch L{};
-  for (int w = 0; w < 2; ++w) L = (rngk ? gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::philox>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err)
-             : gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::compat>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err));
+  for (int w = 0; w < 2; ++w) L = (rngk ? gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::philox, 50>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err)
+             : gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::compat, 50>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err));
   float best = 1e30f, total = 0;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(e0, ctx.stream());
-    L = (rngk ? gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::philox>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err)
-             : gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::compat>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err));
+    L = (rngk ? gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::philox, 50>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err)
+             : gpu::launch_k1<gpu::fn::F4, D, gpu::RngKind::compat, 50>(ctx, f, sh, bin_axes, 123, 0, sh.m, nullptr, err));
     cudaEventRecord(e1, ctx.stream());
     cudaEventSynchronize(e1);
     float ms;
