@@ -179,6 +179,10 @@ struct Launch {
   std::size_t smem = 0;
 };
 
+/// The work-index -> cube map of K1 (see vsample_kernel): whole rows along
+/// axis 0 once there are enough of them.
+inline bool row_mode(const Shape& sh) { return sh.dims >= 2 && sh.m / sh.g >= (std::uint64_t{1} << 20); }
+
 /// Philox4x32-10 key schedule of the iteration key (uniform per launch).
 inline void set_round_keys(SampleArgs& a, std::uint64_t key) {
   std::uint32_t k0 = static_cast<std::uint32_t>(key), k1 = static_cast<std::uint32_t>(key >> 32);
@@ -204,6 +208,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
                  std::uint64_t iter_root, std::uint64_t n0, std::uint64_t n1, const int* stop,
                  unsigned long long* err_key) {
   auto kern = vsample_kernel<F, D, R, NB>;
+  constexpr int kThreads = sample_threads(R, D);
   Launch L;
   L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
   if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
@@ -215,13 +220,13 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   thread_local int cached_occ = 0, cached_dev = -1;
   if (cached_smem != L.smem || cached_dev != ctx.device()) {
     MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)));
-    MCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_occ, kern, kSampleThreads, L.smem));
+    MCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_occ, kern, kThreads, L.smem));
     cached_smem = L.smem;
     cached_dev = ctx.device();
   }
   const int occ = std::max(cached_occ, 1);
   const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
-  const std::uint64_t want = (work + kSampleThreads - 1) / kSampleThreads;
+  const std::uint64_t want = (work + kThreads - 1) / kThreads;
   L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
 
   SampleArgs a{};
@@ -245,18 +250,41 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.n0 = n0;
   a.n1 = n1;
   a.A = sh.A;
-  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kSampleThreads;
-  a.stepT = static_cast<std::uint64_t>((static_cast<unsigned __int128>(T % sh.m) * sh.A) % sh.m);
-  std::uint64_t st = a.stepT;
-  for (int j = 0; j < kMaxDims; ++j) {
-    a.step_digits[j] = j < static_cast<int>(sh.dims) ? st % sh.g : 0;
-    if (j < static_cast<int>(sh.dims)) st /= sh.g;
+  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kThreads;
+  // Row mode when there are >= 2^20 rows (of g cubes along axis 0).  The
+  // n -> cube map must depend on the problem only (m, g, d), never on the
+  // slice [n0, n1) or the launch, so that slices sampled by different ranks
+  // or calls partition the same cube set.
+  const std::uint64_t nrows = D >= 2 ? sh.m / sh.g : 1;
+  a.row_mode = row_mode(sh) ? 1u : 0u;
+  a.R = nrows;
+  if (a.row_mode) {
+    unsigned __int128 Ap = 0, pw = 1;  // A' = 1 + g + ... + g^(D-2) mod R
+    for (int j = 0; j + 1 < D; ++j) {
+      Ap += pw;
+      pw *= sh.g;
+    }
+    a.A = static_cast<std::uint64_t>(Ap % nrows);
+    a.stepR = static_cast<std::uint64_t>((static_cast<unsigned __int128>(T % nrows) * a.A) % nrows);
+    std::uint64_t st = a.stepR;
+    a.step_digits[0] = 0;
+    for (int j = 1; j < kMaxDims; ++j) {
+      a.step_digits[j] = j < D ? st % sh.g : 0;
+      if (j < D) st /= sh.g;
+    }
+  } else {
+    a.stepT = static_cast<std::uint64_t>((static_cast<unsigned __int128>(T % sh.m) * sh.A) % sh.m);
+    std::uint64_t st = a.stepT;
+    for (int j = 0; j < kMaxDims; ++j) {
+      a.step_digits[j] = j < static_cast<int>(sh.dims) ? st % sh.g : 0;
+      if (j < static_cast<int>(sh.dims)) st /= sh.g;
+    }
   }
   a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * (bin_axes * sh.nb) + 1);
   a.scal_partials = ctx.scal_partials.ensure(static_cast<std::size_t>(L.blocks) * kScalarAccs * kXWords);
   a.err_key = err_key;
   a.stop = stop;
-  kern<<<L.blocks, kSampleThreads, L.smem, ctx.stream()>>>(a, f);
+  kern<<<L.blocks, kThreads, L.smem, ctx.stream()>>>(a, f);
   MCB_CUDA(cudaGetLastError());
   ++ctx.launches;
   return L;

@@ -61,9 +61,13 @@ struct SampleArgs {
   double nbpow;    ///< philox: nb^D              (jacobian = nb^D * prod widths)
   std::uint64_t iter_root;  ///< compat: iteration_root(seed, it); philox: the key
   std::uint64_t n0, n1;     ///< this launch's slice of the linear work index
-  std::uint64_t A;          ///< cube(n) = n*A mod m
+  std::uint64_t A;          ///< cube mode: cube(n) = n*A mod m; row mode: rho(r) = r*A mod R
   std::uint64_t stepT;      ///< (gridDim*blockDim*A) mod m
-  std::uint64_t step_digits[kMaxDims];  ///< base-g digits of stepT (axis 0 first)
+  std::uint64_t step_digits[kMaxDims];  ///< cube mode: base-g digits of stepT (axis 0 first);
+                                        ///< row mode: digits of stepR at axes 1..D-1
+  std::uint32_t row_mode;               ///< 1 = walk whole rows along axis 0 (see K1)
+  std::uint64_t R;                      ///< rows m / g
+  std::uint64_t stepR;                  ///< row mode: (T*A) mod R, A = A' = 1 + g + ... + g^(D-2)
   std::uint32_t round_keys[20];         ///< philox: (k0, k1) of rounds 0..9 (uniform; folded into LOP3)
   std::uint32_t* partials;             ///< bins: [gridDim][kXWords][bin_axes*nb] u32
   unsigned long long* scal_partials;   ///< est+/est-/var: [gridDim][3][kXWords] u64 (lane copies folded)
@@ -203,7 +207,7 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
 /// K1.  NB = n_bins when known at compile time (50, the reference default
 /// and every BASELINE config), 0 = runtime n_bins.
 template <class F, int D, RngKind R, int NB = 0>
-__global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const SampleArgs a, const F f) {
+__global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const SampleArgs a, const F f) {
   if (a.stop && *a.stop) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb;
@@ -252,15 +256,76 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
     }
   };
 
+  // ---- work mapping (results do not depend on it: exact sums).
+  //  cube mode: linear index n -> cube t = n*A mod m, thread stride T, all
+  //    digits advanced per cube by an odometer add of (T*A mod m).
+  //  row mode (m/g rows >= 8 threads' worth): n = r*g + e; row r maps to the
+  //    digits of axes 1..D-1 of rho = r*A' mod (m/g), and the thread walks the
+  //    whole row along axis 0 with d0 = (e + digit1(rho)) mod g, so per cube
+  //    only axis 0 changes; rows advance by an odometer add of (T*A' mod m/g).
+  //  Both spread neighbouring lanes over distinct bins on every axis.
+  using Dig = DigitT<D>;
+  const Dig g = static_cast<Dig>(a.g);
   const std::uint64_t T = static_cast<std::uint64_t>(gridDim.x) * nt;
-  std::uint64_t n = a.n0 + static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
-  if (n < a.n1) {
-    using Dig = DigitT<D>;
-    const Dig g = static_cast<Dig>(a.g);
-    std::uint64_t t =
-        static_cast<std::uint64_t>((static_cast<unsigned __int128>(n % a.m) * a.A) % a.m);
-    Dig dig[D];
-    {
+  const std::uint64_t gtid = static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
+  const bool rows = a.row_mode != 0 && D >= 2;
+  std::uint64_t t = 0, n = 0, rp = 0, rowbase = 0, rho = 0;
+  std::uint32_t e = 0, e_end = 0;
+  Dig dig[D];
+  bool active;
+  auto odometer = [&](int j0) {  // dig[j0..D-1] += step_digits[j0..D-1] (mod g, with carries)
+    if constexpr (sizeof(Dig) == 4) {
+      // v = dig + step + carry (< 2g < 2^31); w = v - g; digit = min(v, w)
+      // unsigned; carry = w >= 0, folded into the next axis' add
+      std::uint32_t borrow = 1;  // 1 - carry
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j < j0) continue;
+        const std::uint32_t v = dig[j] + static_cast<std::uint32_t>(a.step_digits[j]) + 1u - borrow;
+        const std::uint32_t w = v - g;
+        dig[j] = v < w ? v : w;
+        borrow = w >> 31;
+      }
+    } else {
+      Dig carry = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j < j0) continue;
+        const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
+        carry = v >= g ? 1 : 0;
+        dig[j] = carry ? v - g : v;
+      }
+    }
+  };
+  // start of a row: e range clipped to [n0, n1), axis-0 digit, cube index
+  auto row_start = [&]() {
+    const std::uint64_t r0 = rp * a.g;
+    e = r0 < a.n0 ? static_cast<std::uint32_t>(a.n0 - r0) : 0u;
+    e_end = static_cast<std::uint32_t>(a.n1 - r0 < a.g ? a.n1 - r0 : a.g);
+    Dig d0 = static_cast<Dig>(e) + dig[1];
+    if (d0 >= g) d0 -= g;
+    dig[0] = d0;
+    rowbase = rho * a.g;
+    t = rowbase + d0;
+  };
+  if (rows) {
+    rp = a.n0 / a.g + gtid;
+    active = rp * a.g < a.n1;
+    if (active) {
+      rho = static_cast<std::uint64_t>((static_cast<unsigned __int128>(rp) * a.A) % a.R);
+      std::uint64_t tt = rho;
+#pragma unroll
+      for (int j = 1; j < D; ++j) {
+        dig[j] = static_cast<Dig>(tt % a.g);
+        tt /= a.g;
+      }
+      row_start();
+    }
+  } else {
+    n = a.n0 + gtid;
+    active = n < a.n1;
+    if (active) {
+      t = static_cast<std::uint64_t>((static_cast<unsigned __int128>(n % a.m) * a.A) % a.m);
       std::uint64_t tt = t;
 #pragma unroll
       for (int j = 0; j < D; ++j) {
@@ -268,93 +333,99 @@ __global__ void __launch_bounds__(kSampleThreads, 1) vsample_kernel(const Sample
         tt /= a.g;
       }
     }
-    const std::uint32_t p = static_cast<std::uint32_t>(a.p);
-    for (; n < a.n1; n += T) {
-      double sum, var;
-      if constexpr (R == RngKind::compat) {
-        double dg[D];
+  }
+  // per-axis cube coordinate: compat = double(digit); philox = digit * nb / g
+  double cd[D];
+  auto coord = [&](int j) {
+    if constexpr (R == RngKind::compat) cd[j] = static_cast<double>(dig[j]);
+    else cd[j] = __dmul_rn(static_cast<double>(dig[j]), a.nbg);
+  };
 #pragma unroll
-        for (int j = 0; j < D; ++j) dg[j] = static_cast<double>(dig[j]);
-        const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
-        double mean = 0.0, m2 = 0.0;
-        sum = 0.0;
-        for (std::uint32_t k = 0; k < p; ++k) {
-          double x[D];
-          std::uint32_t bin[D];
-          double fx;
-          const double fj = sample_point<F, D, NB>(a, f, LW, dg, croot, k, x, bin, fx);
-          if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
-            atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-            continue;
-          }
-          sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
-          // Welford (sampler.hpp:98-103)
-          const std::uint32_t nk = k + 1;
-          const double dd = __dsub_rn(fj, mean);
-          const double q = nk < static_cast<std::uint32_t>(kRcpSmem) ? div_rn(dd, static_cast<double>(nk), rcp[nk])
-                                                                     : __ddiv_rn(dd, static_cast<double>(nk));
-          mean = __dadd_rn(mean, q);
-          m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
-          if (bin_axes) deposit(fj, bin);
-        }
-        var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
-      } else {
-        // Philox path: same estimator (sum of f*J, Welford variance of the
-        // mean), FMA-contracted arithmetic; validated statistically.
-        double base[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) base[j] = __dmul_rn(static_cast<double>(dig[j]), a.nbg);
-        double mean = 0.0, m2 = 0.0;
-        sum = 0.0;
-        for (std::uint32_t k = 0; k < p; ++k) {
-          double x[D];
-          std::uint32_t bin[D];
-          double fx;
-          const double fj = sample_point_fast<F, D, NB>(a, f, LW, base, t, k, x, bin, fx);
-          if (!isfinite(fj)) {
-            atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-            continue;
-          }
-          sum = __dadd_rn(sum, fj);
-          // Welford with y = RN(1/n): mean += (f - mean) * y
-          const std::uint32_t nk = k + 1;
-          const double y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
-          const double dd = __dsub_rn(fj, mean);
-          mean = __fma_rn(dd, y, mean);
-          m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
-          if (bin_axes) deposit(fj, bin);
-        }
-        sum = __dmul_rn(sum, a.scale);
-        var = __dmul_rn(m2, a.rcp_pp1);
-      }
-      if (!(var > 0.0)) var = 0.0;
-      std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
-      exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
+  for (int j = 0; j < D; ++j) coord(j);
 
-      // advance to cube (n + T)*A mod m: odometer add of stepT's digits
+  const std::uint32_t p = static_cast<std::uint32_t>(a.p);
+  while (active) {
+    double sum, var;
+    if constexpr (R == RngKind::compat) {
+      const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
+      double mean = 0.0, m2 = 0.0;
+      sum = 0.0;
+      for (std::uint32_t k = 0; k < p; ++k) {
+        double x[D];
+        std::uint32_t bin[D];
+        double fx;
+        const double fj = sample_point<F, D, NB>(a, f, LW, cd, croot, k, x, bin, fx);
+        if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
+          atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+          continue;
+        }
+        sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
+        // Welford (sampler.hpp:98-103)
+        const std::uint32_t nk = k + 1;
+        const double dd = __dsub_rn(fj, mean);
+        const double q = nk < static_cast<std::uint32_t>(kRcpSmem) ? div_rn(dd, static_cast<double>(nk), rcp[nk])
+                                                                   : __ddiv_rn(dd, static_cast<double>(nk));
+        mean = __dadd_rn(mean, q);
+        m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
+        if (bin_axes) deposit(fj, bin);
+      }
+      var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
+    } else {
+      // Philox path: same estimator (sum of f*J, Welford variance of the
+      // mean), FMA-contracted arithmetic; validated statistically.
+      double mean = 0.0, m2 = 0.0;
+      sum = 0.0;
+      for (std::uint32_t k = 0; k < p; ++k) {
+        double x[D];
+        std::uint32_t bin[D];
+        double fx;
+        const double fj = sample_point_fast<F, D, NB>(a, f, LW, cd, t, k, x, bin, fx);
+        if (!isfinite(fj)) {
+          atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+          continue;
+        }
+        sum = __dadd_rn(sum, fj);
+        // Welford with y = RN(1/n): mean += (f - mean) * y
+        const std::uint32_t nk = k + 1;
+        const double y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
+        const double dd = __dsub_rn(fj, mean);
+        mean = __fma_rn(dd, y, mean);
+        m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
+        if (bin_axes) deposit(fj, bin);
+      }
+      sum = __dmul_rn(sum, a.scale);
+      var = __dmul_rn(m2, a.rcp_pp1);
+    }
+    if (!(var > 0.0)) var = 0.0;
+    std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
+    exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
+
+    // ---- next cube
+    if (rows) {
+      if (++e < e_end) {  // along the row: only axis 0 moves
+        Dig d0 = dig[0] + 1;
+        if (d0 == g) d0 = 0;
+        dig[0] = d0;
+        t = rowbase + d0;
+        coord(0);
+        continue;
+      }
+      rp += T;
+      if (rp * a.g >= a.n1) break;
+      odometer(1);  // rho += T*A' (mod m/g) on the digits of axes 1..D-1
+      rho += a.stepR;
+      if (rho >= a.R) rho -= a.R;
+      row_start();
+    } else {
+      n += T;
+      if (n >= a.n1) break;
+      // cube (n + T)*A mod m: odometer add of stepT's digits
       t += a.stepT;
       if (t >= a.m) t -= a.m;
-      if constexpr (sizeof(Dig) == 4) {
-        // v = dig + step + carry (< 2g < 2^31); w = v - g; digit = min(v, w)
-        // unsigned; carry = w >= 0, folded into the next axis' add
-        std::uint32_t borrow = 1;  // 1 - carry
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const std::uint32_t v = dig[j] + static_cast<std::uint32_t>(a.step_digits[j]) + 1u - borrow;
-          const std::uint32_t w = v - g;
-          dig[j] = v < w ? v : w;
-          borrow = w >> 31;
-        }
-      } else {
-        Dig carry = 0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
-          carry = v >= g ? 1 : 0;
-          dig[j] = carry ? v - g : v;
-        }
-      }
+      odometer(0);
     }
+#pragma unroll
+    for (int j = 0; j < D; ++j) coord(j);
   }
   __syncthreads();
 

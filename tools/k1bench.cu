@@ -61,7 +61,7 @@ int main(int argc, char** argv) {
   std::memcpy(&vb, &h[1], 8);
   const double evals = static_cast<double>(sp.m) * sp.p;
   std::printf("rng=%d frozen=%d threads=%d blocks=%d smem=%zu m=%llu p=%llu best_ms=%.3f avg_ms=%.3f evals/s=%.4e est=%016llx var=%016llx\n",
-              rngk, int(bin_axes == 0), gpu::kSampleThreads, L.blocks, L.smem, (unsigned long long)sp.m, (unsigned long long)sp.p, best,
+              rngk, int(bin_axes == 0), rngk ? gpu::sample_threads(gpu::RngKind::philox, 8) : gpu::kSampleThreads, L.blocks, L.smem, (unsigned long long)sp.m, (unsigned long long)sp.p, best,
               total / reps, evals / (best * 1e-3), (unsigned long long)eb, (unsigned long long)vb);
   return 0;
 }
