@@ -127,9 +127,16 @@ __device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::
 // ---- the same deposits on 32-bit shared-window addresses (atom.shared):
 // no 64-bit generic-pointer arithmetic per axis, and constant per-axis row
 // offsets fold into the instruction's immediate.
+// No "memory" clobber: the accumulators are only read after __syncthreads(),
+// and atomics to distinct words commute, so the compiler may schedule other
+// loads and arithmetic around them.
 __device__ __forceinline__ std::uint32_t atoms_add(std::uint32_t addr, std::uint32_t v) {
   std::uint32_t old;
+#ifdef MCB_ATOMS_MEMCLOBBER
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+#else
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+#endif
   return old;
 }
 

@@ -144,9 +144,9 @@ __device__ __forceinline__ rng::U4 philox_rk(rng::U4 c, const std::uint32_t (&rk
 /// keyed by the iteration with counter (cube, sample, block); bin coordinate
 /// z = (digit + u) * nb / g as one FMA from the per-cube base; point and
 /// jacobian from the {A, width} table.  Returns f*J.
-template <class F, int D, int NB>
+template <class F, int D, int NB, class Dig>
 __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, const double2* LW,
-                                                    const double (&base)[D], std::uint64_t t, std::uint32_t k,
+                                                    const Dig (&dig)[D], std::uint64_t t, std::uint32_t k,
                                                     double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
   const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb, nbm1 = nb - 1;
   std::uint32_t r[(D + 3) & ~3];
@@ -163,8 +163,21 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
   double jw = 1.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    const double z = __fma_rn(__uint2double_rn(r[j]), a.cs, base[j]);
+    // bin coordinate z = (digit + r / 2^32) * nb / g.  For 32-bit digits the
+    // 64-bit integer digit:r (the register pair itself) converts exactly
+    // (digit < 2^21), so z is one I2F.U64 and one DMUL: z = RN((digit 2^32 + r) cs).
+    double z;
+    if constexpr (sizeof(Dig) == 4) {
+      z = __dmul_rn(__ull2double_rn((static_cast<std::uint64_t>(dig[j]) << 32) | r[j]), a.cs);
+    } else {
+      z = __fma_rn(__uint2double_rn(r[j]), a.cs, __dmul_rn(__ull2double_rn(dig[j]), a.nbg));
+    }
+#ifdef MCB_FLOOR_DADD
+    // floor(z) for 0 <= z < 2^31 on the FP64 pipe: RZ(2^52 + z) = 2^52 + floor(z)
+    std::uint32_t i = static_cast<std::uint32_t>(__double2loint(__dadd_rz(z, 0x1.0p52)));
+#else
     std::uint32_t i = __double2uint_rz(z);
+#endif
     i = i < nbm1 ? i : nbm1;
     const double2 lw = LW[j * nb + i];
     x[j] = __fma_rn(z, lw.y, lw.x);
@@ -334,11 +347,10 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       }
     }
   }
-  // per-axis cube coordinate: compat = double(digit); philox = digit * nb / g
-  double cd[D];
+  // compat: per-axis cube coordinate double(digit) (the philox path reads the digits)
+  double cd[R == RngKind::compat ? D : 1];
   auto coord = [&](int j) {
     if constexpr (R == RngKind::compat) cd[j] = static_cast<double>(dig[j]);
-    else cd[j] = __dmul_rn(static_cast<double>(dig[j]), a.nbg);
   };
 #pragma unroll
   for (int j = 0; j < D; ++j) coord(j);
@@ -375,11 +387,14 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       // mean), FMA-contracted arithmetic; validated statistically.
       double mean = 0.0, m2 = 0.0;
       sum = 0.0;
+#ifdef MCB_UNROLL_P
+#pragma unroll 2
+#endif
       for (std::uint32_t k = 0; k < p; ++k) {
         double x[D];
         std::uint32_t bin[D];
         double fx;
-        const double fj = sample_point_fast<F, D, NB>(a, f, LW, cd, t, k, x, bin, fx);
+        const double fj = sample_point_fast<F, D, NB>(a, f, LW, dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
           continue;
@@ -471,9 +486,13 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
   if constexpr (R == RngKind::compat) {
     sample_point<F, D, 0>(a, f, LW, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
   } else {
-    double base[D];
-    for (int j = 0; j < D; ++j) base[j] = __dmul_rn(dg[j], a.nbg);
-    sample_point_fast<F, D, 0>(a, f, LW, base, t, static_cast<std::uint32_t>(k), x, bin, fx);
+    DigitT<D> dig[D];
+    std::uint64_t t2 = t;
+    for (int j = 0; j < D; ++j) {
+      dig[j] = static_cast<DigitT<D>>(t2 % a.g);
+      t2 /= a.g;
+    }
+    sample_point_fast<F, D, 0>(a, f, LW, dig, t, static_cast<std::uint32_t>(k), x, bin, fx);
   }
   for (int j = 0; j < D; ++j) out_x[j] = x[j];
   *out_fx = fx;

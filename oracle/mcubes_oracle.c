@@ -467,10 +467,12 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
   double nbpow = 1.0;
   for (uint32_t j = 0; j < d; ++j) nbpow *= (double)nb;
   double base[64], x[64];
+  uint64_t dig[64];
   uint32_t bin[64], r[68];
   uint64_t tt = t;
   for (uint32_t j = 0; j < d; ++j) {
-    base[j] = (double)(tt % gi) * nbg;
+    dig[j] = tt % gi;
+    base[j] = (double)dig[j] * nbg;
     tt /= gi;
   }
   double sum = 0.0, mean = 0.0, m2 = 0.0;
@@ -482,7 +484,9 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
     }
     double jw = 1.0;
     for (uint32_t j = 0; j < d; ++j) {
-      const double z = fma((double)r[j], cs, base[j]);
+      /* d >= 3: 32-bit digits, z = RN((digit 2^32 + r) * cs) from the exact
+       * 64-bit integer; d <= 2: z = fma(r, cs, RN(digit * nb / g)) */
+      const double z = d >= 3 ? (double)((dig[j] << 32) | r[j]) * cs : fma((double)r[j], cs, base[j]);
       uint32_t i = (uint32_t)z;
       if (i > nb - 1) i = nb - 1;
       const double* row = g->edges + (size_t)j * nb;

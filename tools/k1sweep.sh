@@ -1,6 +1,3 @@
 #!/bin/bash
-# K1 philox threads sweep (k1bench_p<threads> built with -DMCB_SAMPLE_THREADS_PHILOX)
-for b in k1bench_p768 k1bench_p896 k1bench_p1024; do
-  for mc in 10000000000 1000000000; do timeout 120 ./tools/bin/$b $mc 5 1 0; done
-done
-timeout 120 ./tools/bin/k1bench_p768 10000000000 5 0 0
+for b in k1bench k1bench_p1024; do echo -n "$b: "; ./tools/bin/$b 10000000000 3 1 0 4 | tail -1; done
+echo -n "frozen adapted: "; ./tools/bin/k1bench 10000000000 3 1 1 4 | tail -1
