@@ -50,6 +50,11 @@ RNG_DESC = {
               "FMA transform; statistically equivalent to the reference, bitwise equal to its C twin)",
     "compat": "compat (the reference's keyed SplitMix stream and arithmetic order; bitwise equal to the reference)",
 }
+REDUCTIONS = {
+    "philox": "estimate/variance exact (superaccumulator); bins: (f J)^2 rounded to 24 significant bits, "
+              "summed exactly (deterministic, geometry- and GPU-count-independent)",
+    "compat": "exact (superaccumulator), as the reference's ExactSum/ExactBins",
+}
 DATA = {
     "philox": "synthetic (counter-based Philox stream; no input data)",
     "compat": "synthetic (keyed SplitMix stream of the reference; no input data)",
@@ -310,7 +315,7 @@ def run_ours(args, rank, world, local_rank):
                    "n_bins": N_BINS, "maxcalls": args.maxcalls, "m": m, "p": p, "evals_per_step": evals_per_step,
                    "parallelism": f"cube-range partition x{world} + exact all-reduce" if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps", "rng": RNG_DESC[args.rng],
-                   "reductions": "exact (superaccumulator)"},
+                   "reductions": REDUCTIONS[args.rng]},
         "clocks": clk,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * DIMS * N_BINS,

@@ -209,6 +209,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
                  unsigned long long* err_key) {
   auto kern = vsample_kernel<F, D, R, NB>;
   constexpr int kThreads = sample_threads(R, D);
+  constexpr int kWalkers = kThreads;  // threads that walk cubes
   Launch L;
   L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
   if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
@@ -226,7 +227,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   }
   const int occ = std::max(cached_occ, 1);
   const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
-  const std::uint64_t want = (work + kThreads - 1) / kThreads;
+  const std::uint64_t want = (work + kWalkers - 1) / kWalkers;
   L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
 
   SampleArgs a{};
@@ -250,7 +251,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.n0 = n0;
   a.n1 = n1;
   a.A = sh.A;
-  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kThreads;
+  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kWalkers;
   // Row mode when there are >= 2^20 rows (of g cubes along axis 0).  The
   // n -> cube map must depend on the problem only (m, g, d), never on the
   // slice [n0, n1) or the launch, so that slices sampled by different ranks

@@ -176,6 +176,94 @@ __device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::u
   }
 }
 
+// ---- Philox path bin deposits: (f J)^2 rounded to 24 significant bits.
+// The bins only steer the grid adaptation, and shared 32-bit atomics are the
+// K1 throughput ceiling (~7.4 lane-ops/clk/SM on B200, tools/microbench/
+// atoms.cu, conflict-free or not).  With a 24-bit significand (float
+// precision, 6e-8 relative per addend -- far below the Monte Carlo noise of a
+// bin) a deposit spans at most two words, only one when it sits at a word
+// offset <= 8, and the carry out of the upper word is rare (its digit is
+// < 2^23).  The rounding is a pure function of the value and the integer sums
+// stay exact, so results remain independent of launch geometry and GPU count.
+
+/// Two digits of RN24(|v|) * 2^1074 (round-half-up on the 53-bit significand).
+struct Digits2 {
+  std::uint32_t w, d0, d1;
+};
+
+inline constexpr int kBinDrop = 29;  ///< significand bits dropped: 53 - 24
+
+MCB_HD std::uint64_t round_bin_bits(std::uint64_t bits) {
+  return (bits + (1ull << (kBinDrop - 1))) & ~((1ull << kBinDrop) - 1);  // carries into the exponent
+}
+
+MCB_HD bool split_r24(double v, Digits2& out) {
+  std::uint64_t bits;
+#ifdef __CUDA_ARCH__
+  bits = static_cast<std::uint64_t>(__double_as_longlong(v));
+#else
+  std::memcpy(&bits, &v, 8);
+#endif
+  bits &= 0x7fffffffffffffffull;
+  if (!bits) return false;
+  bits = round_bin_bits(bits);
+  const std::uint32_t hi = static_cast<std::uint32_t>(bits >> 32);
+  const std::uint32_t be = hi >> 20;
+  // 24-bit significand m = (implicit:hi[19:0]:lo[31:29]), its LSB at bit pos + 29
+  const std::uint32_t m = (((hi & 0x000FFFFFu) | (be ? 0x00100000u : 0u)) << 3) |
+                          (static_cast<std::uint32_t>(bits) >> kBinDrop);
+  const std::uint32_t pos = (be ? be - 1 : 0) + kBinDrop;
+  const std::uint32_t off = pos & 31u;
+  out.w = pos >> 5;
+  out.d0 = m << off;
+#ifdef __CUDA_ARCH__
+  out.d1 = __funnelshift_l(m, 0u, off);
+#else
+  out.d1 = off ? m >> (32 - off) : 0u;
+#endif
+  return true;
+}
+
+#ifdef __CUDACC__
+/// Predicated shared atomic add (no-op, returns 0, when !on).
+__device__ __forceinline__ std::uint32_t atoms_add_if(std::uint32_t addr, std::uint32_t v, bool on) {
+  std::uint32_t old = 0;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.shared.add.u32 %0, [%1], %2;\n\t}"
+               : "+r"(old)
+               : "r"(addr), "r"(v), "r"(static_cast<std::uint32_t>(on)));
+  return old;
+}
+
+/// Deposit RN24 digits into N accumulators at shared-window addresses a[j]
+/// (= accumulator j + 4 dg.w): two word atomics (predicating the upper one
+/// off when its addend is zero measured slower), a rare ripple above.
+template <int N>
+__device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::uint32_t end, const Digits2& dg) {
+  std::uint32_t t1[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const std::uint32_t o = atoms_add(a[j], dg.d0);
+    // t1 = d1 + carry(o + d0)   (d1 < 2^23: never wraps)
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(t1[j]) : "r"(o), "r"(dg.d0), "r"(dg.d1));
+  }
+  std::uint32_t ripple = 0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+#ifdef MCB_PRED_UPPER
+    const std::uint32_t o = atoms_add_if(a[j] + 4, t1[j], t1[j] != 0);
+#else
+    const std::uint32_t o = atoms_add(a[j] + 4, t1[j]);
+#endif
+    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t1[j]));
+  }
+  if (ripple) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(a[j] + 8, end);
+  }
+}
+#endif
+
 /// Two independent exact adds (the per-cube estimate and variance), issued
 /// interleaved so their atomic round trips overlap.
 __device__ __forceinline__ void add_shared2(std::uint32_t* acc_a, double a, std::uint32_t* acc_b, double b,

@@ -81,7 +81,7 @@ MCB_HD int block_accs(std::uint32_t bin_axes, std::uint32_t nb) {
 }
 
 /// Dynamic shared memory of K1 for a given shape.
-inline std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes) {
+MCB_HD std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes) {
   const std::size_t grid = 2 * sizeof(double) * static_cast<std::size_t>(D) * nb;  // {left, width}
   const std::size_t rcp = sizeof(double) * kRcpSmem;
   std::size_t acc = sizeof(std::uint32_t) * static_cast<std::size_t>(block_accs(bin_axes, nb)) * kXWords;
@@ -217,6 +217,118 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
   return __dmul_rn(fx, jac);
 }
 
+/// The work-index -> cube walk of one K1 thread (results do not depend on
+/// it: the sums are exact and the stream is keyed by cube).
+///  cube mode: linear index n -> cube t = n*A mod m, thread stride T, all
+///    digits advanced per cube by an odometer add of (T*A mod m).
+///  row mode (m/g >= 2^20 rows): n = r*g + e; row r maps to the digits of
+///    axes 1..D-1 of rho = r*A' mod (m/g), and the thread walks the whole row
+///    along axis 0 with d0 = (e + digit1(rho)) mod g, so per cube only axis 0
+///    changes; rows advance by an odometer add of (T*A' mod m/g).
+///  Both spread neighbouring lanes over distinct bins on every axis.
+template <int D>
+struct CubeWalk {
+  using Dig = DigitT<D>;
+  Dig dig[D];
+  std::uint64_t t = 0, n = 0, rp = 0, rowbase = 0, rho = 0;
+  std::uint32_t e = 0, e_end = 0;
+  bool rows = false;
+
+  __device__ __forceinline__ void odometer(const SampleArgs& a, int j0) {  // dig[j0..] += step_digits[j0..]
+    const Dig g = static_cast<Dig>(a.g);
+    if constexpr (sizeof(Dig) == 4) {
+      // v = dig + step + carry (< 2g < 2^31); w = v - g; digit = min(v, w)
+      // unsigned; carry = w >= 0, folded into the next axis' add
+      std::uint32_t borrow = 1;  // 1 - carry
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j < j0) continue;
+        const std::uint32_t v = dig[j] + static_cast<std::uint32_t>(a.step_digits[j]) + 1u - borrow;
+        const std::uint32_t w = v - g;
+        dig[j] = v < w ? v : w;
+        borrow = w >> 31;
+      }
+    } else {
+      Dig carry = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j < j0) continue;
+        const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
+        carry = v >= g ? 1 : 0;
+        dig[j] = carry ? v - g : v;
+      }
+    }
+  }
+  /// start of a row: e range clipped to [n0, n1), axis-0 digit, cube index
+  __device__ __forceinline__ void row_start(const SampleArgs& a) {
+    const Dig g = static_cast<Dig>(a.g);
+    const std::uint64_t r0 = rp * a.g;
+    e = r0 < a.n0 ? static_cast<std::uint32_t>(a.n0 - r0) : 0u;
+    e_end = static_cast<std::uint32_t>(a.n1 - r0 < a.g ? a.n1 - r0 : a.g);
+    Dig d0 = static_cast<Dig>(e) + dig[D >= 2 ? 1 : 0];
+    if (d0 >= g) d0 -= g;
+    dig[0] = d0;
+    rowbase = rho * a.g;
+    t = rowbase + d0;
+  }
+  /// First cube of global thread gtid; false if it has none.
+  __device__ __forceinline__ bool init(const SampleArgs& a, std::uint64_t gtid) {
+    rows = a.row_mode != 0 && D >= 2;
+    if (rows) {
+      rp = a.n0 / a.g + gtid;
+      if (rp * a.g >= a.n1) return false;
+      rho = static_cast<std::uint64_t>((static_cast<unsigned __int128>(rp) * a.A) % a.R);
+      std::uint64_t tt = rho;
+#pragma unroll
+      for (int j = 1; j < D; ++j) {
+        dig[j] = static_cast<Dig>(tt % a.g);
+        tt /= a.g;
+      }
+      row_start(a);
+      return true;
+    }
+    n = a.n0 + gtid;
+    if (n >= a.n1) return false;
+    t = static_cast<std::uint64_t>((static_cast<unsigned __int128>(n % a.m) * a.A) % a.m);
+    std::uint64_t tt = t;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      dig[j] = static_cast<Dig>(tt % a.g);
+      tt /= a.g;
+    }
+    return true;
+  }
+  /// Advance by the thread stride T; false when done.  all_axes = false when
+  /// only dig[0] changed.
+  __device__ __forceinline__ bool next(const SampleArgs& a, std::uint64_t T, bool& all_axes) {
+    all_axes = true;
+    if (rows) {
+      if (++e < e_end) {  // along the row: only axis 0 moves
+        Dig d0 = dig[0] + 1;
+        if (d0 == static_cast<Dig>(a.g)) d0 = 0;
+        dig[0] = d0;
+        t = rowbase + d0;
+        all_axes = false;
+        return true;
+      }
+      rp += T;
+      if (rp * a.g >= a.n1) return false;
+      odometer(a, 1);  // rho += T*A' (mod m/g) on the digits of axes 1..D-1
+      rho += a.stepR;
+      if (rho >= a.R) rho -= a.R;
+      row_start(a);
+      return true;
+    }
+    n += T;
+    if (n >= a.n1) return false;
+    // cube (n + T)*A mod m: odometer add of stepT's digits
+    t += a.stepT;
+    if (t >= a.m) t -= a.m;
+    odometer(a, 0);
+    return true;
+  }
+};
+
 /// K1.  NB = n_bins when known at compile time (50, the reference default
 /// and every BASELINE config), 0 = runtime n_bins.
 template <class F, int D, RngKind R, int NB = 0>
@@ -253,110 +365,44 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
 
   // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once,
   // deposit word-major across the axes
+  // (compat: the exact (f J)^2, as the reference's ExactBins; philox: rounded
+  // to 24 significant bits -- one or two word atomics instead of three, exact.cuh)
   auto deposit = [&](double fj, const std::uint32_t (&bin)[D]) {
-    exact::Digits dgt;
-    if (exact::split(__dmul_rn(fj, fj), dgt)) {
+    using Dg = std::conditional_t<R == RngKind::compat, exact::Digits, exact::Digits2>;
+    Dg dgt;
+    bool nz;
+    if constexpr (R == RngKind::compat) nz = exact::split(__dmul_rn(fj, fj), dgt);
+    else nz = exact::split_r24(__dmul_rn(fj, fj), dgt);
+    if (nz) {
       const std::uint32_t wb = bins_s + 4u * dgt.w;
       if (bin_axes == static_cast<std::uint32_t>(D)) {
         std::uint32_t ad[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
-        exact::add_digits_s<D>(ad, end_s, dgt);
+        if constexpr (R == RngKind::compat) exact::add_digits_s<D>(ad, end_s, dgt);
+        else exact::add_digits2_s<D>(ad, end_s, dgt);
       } else {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
-        exact::add_digits_s<1>(ad, end_s, dgt);
+        if constexpr (R == RngKind::compat) exact::add_digits_s<1>(ad, end_s, dgt);
+        else exact::add_digits2_s<1>(ad, end_s, dgt);
       }
     }
   };
 
-  // ---- work mapping (results do not depend on it: exact sums).
-  //  cube mode: linear index n -> cube t = n*A mod m, thread stride T, all
-  //    digits advanced per cube by an odometer add of (T*A mod m).
-  //  row mode (m/g rows >= 8 threads' worth): n = r*g + e; row r maps to the
-  //    digits of axes 1..D-1 of rho = r*A' mod (m/g), and the thread walks the
-  //    whole row along axis 0 with d0 = (e + digit1(rho)) mod g, so per cube
-  //    only axis 0 changes; rows advance by an odometer add of (T*A' mod m/g).
-  //  Both spread neighbouring lanes over distinct bins on every axis.
-  using Dig = DigitT<D>;
-  const Dig g = static_cast<Dig>(a.g);
   const std::uint64_t T = static_cast<std::uint64_t>(gridDim.x) * nt;
-  const std::uint64_t gtid = static_cast<std::uint64_t>(blockIdx.x) * nt + tid;
-  const bool rows = a.row_mode != 0 && D >= 2;
-  std::uint64_t t = 0, n = 0, rp = 0, rowbase = 0, rho = 0;
-  std::uint32_t e = 0, e_end = 0;
-  Dig dig[D];
-  bool active;
-  auto odometer = [&](int j0) {  // dig[j0..D-1] += step_digits[j0..D-1] (mod g, with carries)
-    if constexpr (sizeof(Dig) == 4) {
-      // v = dig + step + carry (< 2g < 2^31); w = v - g; digit = min(v, w)
-      // unsigned; carry = w >= 0, folded into the next axis' add
-      std::uint32_t borrow = 1;  // 1 - carry
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (j < j0) continue;
-        const std::uint32_t v = dig[j] + static_cast<std::uint32_t>(a.step_digits[j]) + 1u - borrow;
-        const std::uint32_t w = v - g;
-        dig[j] = v < w ? v : w;
-        borrow = w >> 31;
-      }
-    } else {
-      Dig carry = 0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (j < j0) continue;
-        const Dig v = dig[j] + static_cast<Dig>(a.step_digits[j]) + carry;
-        carry = v >= g ? 1 : 0;
-        dig[j] = carry ? v - g : v;
-      }
-    }
-  };
-  // start of a row: e range clipped to [n0, n1), axis-0 digit, cube index
-  auto row_start = [&]() {
-    const std::uint64_t r0 = rp * a.g;
-    e = r0 < a.n0 ? static_cast<std::uint32_t>(a.n0 - r0) : 0u;
-    e_end = static_cast<std::uint32_t>(a.n1 - r0 < a.g ? a.n1 - r0 : a.g);
-    Dig d0 = static_cast<Dig>(e) + dig[1];
-    if (d0 >= g) d0 -= g;
-    dig[0] = d0;
-    rowbase = rho * a.g;
-    t = rowbase + d0;
-  };
-  if (rows) {
-    rp = a.n0 / a.g + gtid;
-    active = rp * a.g < a.n1;
-    if (active) {
-      rho = static_cast<std::uint64_t>((static_cast<unsigned __int128>(rp) * a.A) % a.R);
-      std::uint64_t tt = rho;
-#pragma unroll
-      for (int j = 1; j < D; ++j) {
-        dig[j] = static_cast<Dig>(tt % a.g);
-        tt /= a.g;
-      }
-      row_start();
-    }
-  } else {
-    n = a.n0 + gtid;
-    active = n < a.n1;
-    if (active) {
-      t = static_cast<std::uint64_t>((static_cast<unsigned __int128>(n % a.m) * a.A) % a.m);
-      std::uint64_t tt = t;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        dig[j] = static_cast<Dig>(tt % a.g);
-        tt /= a.g;
-      }
-    }
-  }
+  CubeWalk<D> cw;
+  bool active = cw.init(a, static_cast<std::uint64_t>(blockIdx.x) * nt + tid);
   // compat: per-axis cube coordinate double(digit) (the philox path reads the digits)
   double cd[R == RngKind::compat ? D : 1];
   auto coord = [&](int j) {
-    if constexpr (R == RngKind::compat) cd[j] = static_cast<double>(dig[j]);
+    if constexpr (R == RngKind::compat) cd[j] = static_cast<double>(cw.dig[j]);
   };
 #pragma unroll
   for (int j = 0; j < D; ++j) coord(j);
 
   const std::uint32_t p = static_cast<std::uint32_t>(a.p);
   while (active) {
+    const std::uint64_t t = cw.t;
     double sum, var;
     if constexpr (R == RngKind::compat) {
       const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
@@ -387,14 +433,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       // mean), FMA-contracted arithmetic; validated statistically.
       double mean = 0.0, m2 = 0.0;
       sum = 0.0;
-#ifdef MCB_UNROLL_P
-#pragma unroll 2
-#endif
       for (std::uint32_t k = 0; k < p; ++k) {
         double x[D];
         std::uint32_t bin[D];
         double fx;
-        const double fj = sample_point_fast<F, D, NB>(a, f, LW, dig, t, k, x, bin, fx);
+        const double fj = sample_point_fast<F, D, NB>(a, f, LW, cw.dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
           continue;
@@ -415,32 +458,14 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
     exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
 
-    // ---- next cube
-    if (rows) {
-      if (++e < e_end) {  // along the row: only axis 0 moves
-        Dig d0 = dig[0] + 1;
-        if (d0 == g) d0 = 0;
-        dig[0] = d0;
-        t = rowbase + d0;
-        coord(0);
-        continue;
-      }
-      rp += T;
-      if (rp * a.g >= a.n1) break;
-      odometer(1);  // rho += T*A' (mod m/g) on the digits of axes 1..D-1
-      rho += a.stepR;
-      if (rho >= a.R) rho -= a.R;
-      row_start();
-    } else {
-      n += T;
-      if (n >= a.n1) break;
-      // cube (n + T)*A mod m: odometer add of stepT's digits
-      t += a.stepT;
-      if (t >= a.m) t -= a.m;
-      odometer(0);
-    }
+    bool all_axes;
+    active = cw.next(a, T, all_axes);
+    if (all_axes) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) coord(j);
+      for (int j = 0; j < D; ++j) coord(j);
+    } else {
+      coord(0);
+    }
   }
   __syncthreads();
 

@@ -512,8 +512,12 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
     const uint64_t nk = k + 1;
     mean = fma(dd, 1.0 / (double)nk, mean);
     m2 = fma(dd, fj - mean, m2);
-    if (kbins) {
-      const double sq = fj * fj;
+    if (kbins) { /* (f J)^2 rounded half-up to 24 significant bits (exact.cuh split_r24) */
+      double sq = fj * fj;
+      uint64_t b;
+      memcpy(&b, &sq, 8);
+      b = (b + (1ull << 28)) & ~((1ull << 29) - 1);
+      memcpy(&sq, &b, 8);
       for (uint32_t j = 0; j < bin_axes; ++j) xacc_add_mag(&acc->bins[(size_t)j * nb + bin[j]], sq);
       acc->writes += bin_axes;
     }
