@@ -132,11 +132,14 @@ class Context {
     MCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
     stream_ = own_stream_;
     MCB_CUDA(cudaMallocHost(&pinned_, kPinnedBytes));
+    MCB_CUDA(cudaMallocHost(&flags_, sizeof(int) * kMaxFlagIterations));
   }
   ~Context() {
     cudaSetDevice(device_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
     if (pinned_) cudaFreeHost(pinned_);
+    if (flags_) cudaFreeHost(flags_);
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
   }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
@@ -164,6 +167,20 @@ class Context {
   static constexpr std::size_t kPinnedBytes = 1 << 20;
   unsigned char* pinned() const { return pinned_; }
 
+  /// Host-mapped per-iteration progress flags written by the finish kernel
+  /// (0 = not run, 1 = continue, 2 = stop), for integrate()'s bounded lookahead.
+  static constexpr std::uint32_t kMaxFlagIterations = 16384;
+  int* host_flags() const { return flags_; }
+  /// The i-th event of a reusable pool (created on first use).
+  cudaEvent_t event(std::size_t i) {
+    while (events_.size() <= i) {
+      cudaEvent_t e;
+      MCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      events_.push_back(e);
+    }
+    return events_[i];
+  }
+
  private:
   int device_ = 0;
   int sms_ = 0;
@@ -171,13 +188,19 @@ class Context {
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t stream_ = nullptr;
   unsigned char* pinned_ = nullptr;
+  int* flags_ = nullptr;
+  std::vector<cudaEvent_t> events_;
 };
 
 /// Geometry of one K1 launch (results do not depend on it).
 struct Launch {
   int blocks = 0;
   std::size_t smem = 0;
+  std::uint32_t pnb = 0;  ///< partial cells per axis (n_bins, +1 padding cell on the Philox path)
 };
+
+/// Cells per axis in K1's shared histogram and partials for a stream kind.
+constexpr std::uint32_t partial_bins(RngKind r, std::uint32_t nb) { return nb + (r == RngKind::philox ? 1u : 0u); }
 
 /// The work-index -> cube map of K1 (see vsample_kernel): whole rows along
 /// axis 0 once there are enough of them.
@@ -211,7 +234,8 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   constexpr int kThreads = sample_threads(R, D);
   constexpr int kWalkers = kThreads;  // threads that walk cubes
   Launch L;
-  L.smem = sample_smem_bytes(D, sh.nb, bin_axes);
+  L.pnb = partial_bins(R, sh.nb);
+  L.smem = sample_smem_bytes(D, L.pnb, bin_axes);
   if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
     throw std::invalid_argument("B200 path: dims*n_bins too large for the shared-memory histogram (" +
                                 std::to_string(L.smem) + " B > " + std::to_string(ctx.max_smem()) + " B)");
@@ -281,7 +305,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
       if (j < static_cast<int>(sh.dims)) st /= sh.g;
     }
   }
-  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * (bin_axes * sh.nb) + 1);
+  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * (bin_axes * L.pnb) + 1);
   a.scal_partials = ctx.scal_partials.ensure(static_cast<std::size_t>(L.blocks) * kScalarAccs * kXWords);
   a.err_key = err_key;
   a.stop = stop;
@@ -308,7 +332,7 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
   set_fast_constants(a, sh, D);
   a.iter_root = iter_root;
   set_round_keys(a, iter_root);
-  const std::size_t smem = 2 * sizeof(double) * D * sh.nb;
+  const std::size_t smem = 2 * sizeof(double) * D * partial_bins(R, sh.nb);
   auto kern = sample_point_kernel<F, D, R>;
   MCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<1, 128, smem, ctx.stream()>>>(a, f, t, k, out_x, out_fx);
@@ -366,10 +390,13 @@ inline void launch_reduce(Context& ctx, const Launch& L, std::uint32_t bin_axes,
   const int nbins = static_cast<int>(bin_axes * nb);
   const int n = (nbins + kScalarAccs) * kXWords;
   MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * n, ctx.stream()));
+  const std::uint32_t pnb = L.pnb ? L.pnb : nb;
+  const int npart = (static_cast<int>(bin_axes * pnb) + kScalarAccs) * kXWords;
   const int chunks = std::max(1, std::min(L.blocks, 16));
-  const dim3 grid((n + 255) / 256, chunks);
+  const dim3 grid((npart + 255) / 256, chunks);
   reduce_partials_kernel<0><<<grid, 256, 0, ctx.stream()>>>(ctx.partials.get(), ctx.scal_partials.get(), L.blocks,
-                                                             nbins, words, stop);
+                                                             static_cast<int>(bin_axes * pnb), static_cast<int>(pnb),
+                                                             static_cast<int>(nb), words, stop);
   MCB_CUDA(cudaGetLastError());
   ++ctx.launches;
 }

@@ -46,9 +46,11 @@ MCB_HD int exchange_accs(std::uint32_t bin_axes, std::uint32_t nb) {
 /// K3a sums them over blocks into the exchange buffer (zeroed beforehand).
 /// Blocks are split into `gridDim.y` chunks whose sums meet in 64-bit integer
 /// atomics: integer addition, so exact and order-free.
+/// Partial slots c = axis*pnb + cell; cells >= nb (the Philox path's padding
+/// cell) fold into bin nb-1 of the exchange buffer.
 template <int kTag = 0>
 __global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ bins, const unsigned long long* __restrict__ scal,
-                                       int nblocks, int nbins, unsigned long long* __restrict__ words,
+                                       int nblocks, int nbins, int pnb, int nb, unsigned long long* __restrict__ words,
                                        const int* stop) {
   if (stop && *stop) return;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -67,7 +69,9 @@ __global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ bins, c
     if (b < b1) s0 += bins[b * stride + idx];
     const unsigned long long s = s0 + s1;
     const int w = idx / nbins, c = idx % nbins;
-    if (s) atomicAdd(words + (kScalarAccs + c) * kXWords + w, s);
+    const int ax = c / pnb, cell = c % pnb;
+    const int slot = ax * nb + (cell < nb ? cell : nb - 1);
+    if (s) atomicAdd(words + (kScalarAccs + slot) * kXWords + w, s);
   } else {  // idx - nbin_words = kind * kXWords + w
     const int j = idx - nbin_words;
     for (int b = b0; b < b1; ++b) s0 += scal[static_cast<std::size_t>(b) * nscal_words + j];
@@ -292,6 +296,7 @@ struct EpilogueArgs {
   int adj_warps;  ///< warps with adaptation scratch (set by launch_finish)
   double tau, chi2max;
   AdjustArgs adj;
+  int* host_flags;  ///< nullable, host-mapped: [it-1] = 1 (continue) or 2 (stop) once this iteration finished
 };
 
 inline constexpr int kFinishThreads = 512;
@@ -351,6 +356,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
       st->failed = 1;
       st->failed_iteration = e.it;
       st->stop = 1;
+      if (e.host_flags) e.host_flags[e.it - 1] = 2;
     }
     return;
   }
@@ -366,6 +372,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
       st->converged = 1;
       st->stop = 1;
     }
+    if (e.host_flags) e.host_flags[e.it - 1] = st->stop ? 2 : 1;
   }
 }
 

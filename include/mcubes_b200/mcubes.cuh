@@ -624,6 +624,9 @@ class Run {
     return static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
   }
   unsigned long long* exchange() const { return words_; }
+  /// Have finish() report per-iteration progress into host-mapped flags
+  /// (Context::host_flags layout); nullptr turns it off.
+  void set_host_flags(int* f) { host_flags_ = f; }
   /// Use a caller-owned exchange buffer (e.g. a torch tensor the caller all-reduces).
   void set_exchange(unsigned long long* p) { words_ = p ? p : ctx_.words.get(); }
   const int* stop_flag() const { return &ctx_.state.get()->stop; }
@@ -659,6 +662,7 @@ class Run {
                        ctx_.edges.get(), ctx_.contrib.get(),
                        cfg_.alpha,       cfg_.variant == Variant::mcubes1d ? 1 : 0,
                        ctx_.contrib.get()};
+    e.host_flags = host_flags_;
     launch_finish(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
                   ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e);
   }
@@ -723,6 +727,7 @@ class Run {
   unsigned long long* words_ = nullptr;
   Launch last_{};
   std::uint32_t last_it_ = 0;
+  int* host_flags_ = nullptr;
 };
 
 /// integrate() for type-erased integrands: the whole schedule is enqueued
@@ -730,10 +735,28 @@ class Run {
 inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, const RunConfig& cfg,
                                        const IterationObserver& observe = {}) {
   Run run(ctx, ops, cfg);
+  // Bounded lookahead: keep at most kAhead iterations in flight and stop
+  // enqueuing once the finish kernel has reported convergence through the
+  // host-mapped flags, so a run that converges early does not pay for the
+  // launches of its remaining (no-op) iterations.  Results are unaffected:
+  // iterations after `stop` are no-ops on the device either way.
+  constexpr std::uint32_t kAhead = 2;
+  const bool lookahead = !observe && cfg.itmax <= Context::kMaxFlagIterations;
+  int* flags = ctx.host_flags();
+  if (lookahead) {
+    std::memset(flags, 0, sizeof(int) * cfg.itmax);
+    run.set_host_flags(flags);
+  }
   for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
+    if (lookahead && it > kAhead) {
+      const std::uint32_t back = it - kAhead;
+      MCB_CUDA(cudaEventSynchronize(ctx.event(back % (kAhead + 1))));
+      if (reinterpret_cast<volatile int*>(flags)[back - 1] != 1) break;  // stopped (or never ran: stopped earlier)
+    }
     run.sample(it);
     run.reduce(it);
     run.finish(it);
+    if (lookahead) MCB_CUDA(cudaEventRecord(ctx.event(it % (kAhead + 1)), ctx.stream()));
     if (observe) {
       const RunState st = run.state();
       if (st.failed || st.iterations_used != it) break;

@@ -115,11 +115,15 @@ __device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
 /// Philox path: per-bin {A, width} with A = left - i*width, so the point is
 /// one FMA of the bin coordinate z: x = A + z*width (= left + (z-i)*width up
 /// to one rounding).
+/// The table has nb + 1 entries per axis: entry nb repeats bin nb-1, so a
+/// bin coordinate that rounds up to exactly nb (possible only for g >= 2^20)
+/// needs no clamp -- its deposit lands in a padding cell that K3a folds into
+/// bin nb-1 (philox_pnb).
 template <int D>
 __device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a) {
-  const std::uint32_t nb = a.nb;
-  for (std::uint32_t idx = threadIdx.x; idx < D * nb; idx += blockDim.x) {
-    const std::uint32_t j = idx / nb, i = idx % nb;
+  const std::uint32_t nb = a.nb, pnb = nb + 1;
+  for (std::uint32_t idx = threadIdx.x; idx < D * pnb; idx += blockDim.x) {
+    const std::uint32_t j = idx / pnb, i0 = idx % pnb, i = i0 < nb ? i0 : nb - 1;
     const double* row = a.edges + static_cast<std::size_t>(j) * nb;
     const double left = i == 0 ? a.lower[j] : row[i - 1];
     const double w = __dsub_rn(row[i], left);
@@ -148,7 +152,7 @@ template <class F, int D, int NB, class Dig>
 __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, const double2* LW,
                                                     const Dig (&dig)[D], std::uint64_t t, std::uint32_t k,
                                                     double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
-  const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb, nbm1 = nb - 1;
+  const std::uint32_t pnb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + 1;  // padded table (stage_grid_fast)
   std::uint32_t r[(D + 3) & ~3];
 #pragma unroll
   for (int q = 0; q < (D + 3) / 4; ++q) {
@@ -172,14 +176,8 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
     } else {
       z = __fma_rn(__uint2double_rn(r[j]), a.cs, __dmul_rn(__ull2double_rn(dig[j]), a.nbg));
     }
-#ifdef MCB_FLOOR_DADD
-    // floor(z) for 0 <= z < 2^31 on the FP64 pipe: RZ(2^52 + z) = 2^52 + floor(z)
-    std::uint32_t i = static_cast<std::uint32_t>(__double2loint(__dadd_rz(z, 0x1.0p52)));
-#else
-    std::uint32_t i = __double2uint_rz(z);
-#endif
-    i = i < nbm1 ? i : nbm1;
-    const double2 lw = LW[j * nb + i];
+    const std::uint32_t i = __double2uint_rz(z);  // 0 <= z <= nb: no clamp (padded table)
+    const double2 lw = LW[j * pnb + i];
     x[j] = __fma_rn(z, lw.y, lw.x);
     jw = j == 0 ? lw.y : __dmul_rn(jw, lw.y);
     bin[j] = i;
@@ -335,7 +333,8 @@ template <class F, int D, RngKind R, int NB = 0>
 __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const SampleArgs a, const F f) {
   if (a.stop && *a.stop) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb;
+  // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
+  const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (R == RngKind::philox ? 1u : 0u);
   double2* LW = reinterpret_cast<double2*>(smem);
   double* rcp = reinterpret_cast<double*>(LW + D * nb);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
