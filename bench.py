@@ -451,6 +451,8 @@ def run_suite(path: str):
 
     def gpu_run(f, cfg, reps=3):
         M.integrate(f, cfg, ctx=ctx)
+        if cfg.maxcalls >= 10 ** 10:
+            reps = 1  # seconds per run already; the warm-up above loaded everything
         best, r = 1e30, None
         for _ in range(reps):
             torch.cuda.synchronize()
@@ -469,10 +471,18 @@ def run_suite(path: str):
         hi = hi or [1.0] * d
         cfg = M.RunConfig(dims=d, maxcalls=mc, itmax=itmax, ita=ita, tau_rel=tau, seed=seed, lower=lo, upper=hi)
         r, gms = gpu_run(f, cfg)
+        cfgp = M.RunConfig(dims=d, maxcalls=mc, itmax=itmax, ita=ita, tau_rel=tau, seed=seed, lower=lo, upper=hi,
+                           rng="philox")
+        rp, pms = gpu_run(f, cfgp)
         row = dict(config=config, integrand=name, dims=d, maxcalls=mc, itmax=itmax, ita=ita, tau_rel=tau, seed=seed,
                    evals=r.total_samples, gpu_ms=gms, gpu_evals_per_s=r.total_samples / (gms * 1e-3),
                    gpu_iterations=r.iterations_used, gpu_converged=r.converged, gpu_estimate=r.estimate,
-                   gpu_sigma=r.sigma, gpu_chi2_dof=r.chi2_dof, truth=f.reference)
+                   gpu_sigma=r.sigma, gpu_chi2_dof=r.chi2_dof, truth=f.reference,
+                   philox_ms=pms, philox_evals=rp.total_samples, philox_evals_per_s=rp.total_samples / (pms * 1e-3),
+                   philox_iterations=rp.iterations_used, philox_converged=rp.converged, philox_estimate=rp.estimate,
+                   philox_sigma=rp.sigma, philox_chi2_dof=rp.chi2_dof)
+        if f.reference is not None and rp.sigma > 0:
+            row["philox_pull_vs_truth"] = (rp.estimate - f.reference) / rp.sigma
         if cpu:
             o, cms = cpu_run(fid, params, d, mc, itmax, ita, tau, seed, lo, hi)
             row.update(cpu_ms=cms, cpu_threads=threads, cpu_iterations=o["iterations_used"],
@@ -480,7 +490,10 @@ def run_suite(path: str):
                        speedup=cms / gms, same_iterations=o["iterations_used"] == r.iterations_used,
                        same_convergence=o["converged"] == r.converged,
                        estimate_bitwise_equal=o["estimate"] == r.estimate,
-                       within_3_combined_sigma=abs(o["estimate"] - r.estimate) <= 3 * math.hypot(o["sigma"], r.sigma))
+                       within_3_combined_sigma=abs(o["estimate"] - r.estimate) <= 3 * math.hypot(o["sigma"], r.sigma),
+                       philox_speedup=cms / pms,
+                       philox_within_3_combined_sigma=abs(o["estimate"] - rp.estimate)
+                       <= 3 * math.hypot(o["sigma"], rp.sigma))
         emit(row)
 
     # C1: 5D f4, ncall 1e6, 10 iterations (the reference's CPU-runnable case)
@@ -507,6 +520,8 @@ def run_suite(path: str):
     for dd in (2, 4, 6, 8, 10):
         for mc in (10 ** 6, 10 ** 8, 10 ** 10):
             both("C5", "f4", M.make_suite_integrand(4, dd), 4, None, dd, mc, 5, 3, 1e-15, cpu=mc <= 10 ** 8)
+    for dd in (2, 6, 8):  # the top of the ncall range, GPU only
+        both("C5", "f4", M.make_suite_integrand(4, dd), 4, None, dd, 10 ** 11, 3, 2, 1e-15, cpu=False)
     out.close()
 
 
