@@ -386,10 +386,10 @@ void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t ite
 /// K3a: per-block partials -> exchange words (zeroed first; chunks of blocks
 /// meet in exact 64-bit integer atomics).
 inline void launch_reduce(Context& ctx, const Launch& L, std::uint32_t bin_axes, std::uint32_t nb,
-                          unsigned long long* words, const int* stop) {
+                          unsigned long long* words, const int* stop, bool words_zeroed = false) {
   const int nbins = static_cast<int>(bin_axes * nb);
   const int n = (nbins + kScalarAccs) * kXWords;
-  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * n, ctx.stream()));
+  if (!words_zeroed) MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * n, ctx.stream()));
   const std::uint32_t pnb = L.pnb ? L.pnb : nb;
   const int npart = (static_cast<int>(bin_axes * pnb) + kScalarAccs) * kXWords;
   const int chunks = std::max(1, std::min(L.blocks, 16));
@@ -416,8 +416,9 @@ inline int adjust_warps(std::uint32_t dims, std::uint32_t nb, int max_smem) {
 
 /// K3b + K4 fused: exchange words -> estimate, variance, contributions; with
 /// an epilogue, also grid adaptation + weighted estimate + convergence.
-inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes, const unsigned long long* words,
-                          double* est, double* var, double* contrib, const int* stop, const EpilogueArgs* epi) {
+inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes, unsigned long long* words,
+                          double* est, double* var, double* contrib, const int* stop, const EpilogueArgs* epi,
+                          bool zero_words = false) {
   RoundArgs r{};
   r.words = words;
   r.dims = sh.dims;
@@ -428,6 +429,7 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   r.var = var;
   r.contrib = contrib;
   r.stop = stop;
+  r.zero_words = (zero_words && epi) ? 1 : 0;
   EpilogueArgs e{};
   std::size_t smem = 0;
   if (epi) {

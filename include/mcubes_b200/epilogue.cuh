@@ -94,6 +94,26 @@ __global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ bins, c
 ///   * the edge is left + width * ((T[i] - P[k]) / imp[k]) as in the reference.
 /// The nextafter repair passes run sequentially only if some edge needs one.
 /// scratch: kAdjustScratch * n doubles.  contrib must be finite and >= 0.
+#ifdef MCB_FINISH_TIMING
+// latency probe (tools/latbench.cu): %globaltimer at the finish kernel's phases
+__device__ unsigned long long g_fin_times[16];
+__device__ __forceinline__ unsigned long long fin_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MCB_FIN_STAMP(i) g_fin_times[i] = fin_now()
+#define MCB_FIN_STAMP_MAX(i) atomicMax(&g_fin_times[i], fin_now())
+#else
+#define MCB_FIN_STAMP(i)
+#define MCB_FIN_STAMP_MAX(i)
+#endif
+#ifdef MCB_FINISH_TIMING
+#define MCB_ADJ_STAMP(i) if (threadIdx.x == 0) g_fin_times[8 + (i)] = fin_now()
+#else
+#define MCB_ADJ_STAMP(i)
+#endif
+
 inline constexpr int kAdjustScratch = 6;  ///< doubles per bin of per-warp scratch
 
 __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, const double* contrib,
@@ -110,6 +130,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     any_local |= contrib[i] != 0.0;
   }
   const bool any = __any_sync(0xffffffffu, any_local);
+  MCB_ADJ_STAMP(0);
   if (!any || n == 1) return;  // nothing observed: leave the axis alone
   for (std::uint32_t i = lane; i < n; i += 32) {
     double s;
@@ -125,6 +146,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     for (std::uint32_t i = 0; i < n; ++i) total += smooth[i];
   }
   total = __shfl_sync(0xffffffffu, total, 0);
+  MCB_ADJ_STAMP(1);
   for (std::uint32_t i = lane; i < n; i += 32) {
     const double c = smooth[i] / total;
     double r = 0.0;
@@ -133,6 +155,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     imp[i] = r;
   }
   __syncwarp();
+  MCB_ADJ_STAMP(2);
   if (lane == 0) {  // the reference's sequential accumulations, in its order
     // rtot (grid.hpp:603-613) and the walk's cum (grid.hpp:623-626) add the
     // same imp[] in the same order, so one pass yields both: P[n] == rtot.
@@ -152,6 +175,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     }
   }
   __syncwarp();
+  MCB_ADJ_STAMP(3);
   double* out = smooth;  // smooth is dead: reuse it as the output row
   for (std::uint32_t i = lane; i + 1 < n; i += 32) {
     const double t = T[i];
@@ -171,6 +195,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     out[i] = left + width * ((t - P[k]) / imp[k]);
   }
   __syncwarp();
+  MCB_ADJ_STAMP(4);
   bool bad = false;
   for (std::uint32_t i = lane; i + 1 < n; i += 32) {
     const double prev = i == 0 ? lo : out[i - 1];
@@ -190,8 +215,10 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
     }
   }
   __syncwarp();
+  MCB_ADJ_STAMP(5);
   for (std::uint32_t i = lane; i < n; i += 32) edges_g[i] = i + 1 < n ? out[i] : hi;
   __syncwarp();
+  MCB_ADJ_STAMP(6);
 }
 
 struct AdjustArgs {
@@ -241,6 +268,57 @@ __global__ void adjust_grid_kernel(const AdjustArgs a) {
   adjust_grid_block(a, a.contrib, adj_scratch, blockDim.x >> 5);
 }
 
+#ifdef __CUDACC__
+/// weighted_estimate_dev by one warp, bit-identical: the loads, reciprocals
+/// and per-iteration terms are lane-parallel; the three sums are accumulated
+/// by lane 0 in the reference's left-to-right order.  All lanes return the
+/// results.
+__device__ inline void weighted_estimate_warp(const double* est, const double* var, std::uint32_t n, double& mean,
+                                              double& sigma, double& chi2_dof) {
+  const int lane = threadIdx.x & 31;
+  // first iteration with zero variance (driver.hpp:148-153)
+  int zero_at = -1;
+  for (std::uint32_t b = 0; b < n && zero_at < 0; b += 32) {
+    const std::uint32_t i = b + lane;
+    const unsigned z = __ballot_sync(0xffffffffu, i < n && var[i] == 0.0);
+    if (z) zero_at = static_cast<int>(b) + __ffs(z) - 1;
+  }
+  if (zero_at >= 0) {
+    mean = est[zero_at];
+    sigma = 0.0;
+    chi2_dof = 0.0;
+    return;
+  }
+  double sum_w = 0.0, sum_wi = 0.0;
+  for (std::uint32_t b = 0; b < n; b += 32) {
+    const std::uint32_t i = b + lane;
+    const double w = i < n ? 1.0 / var[i] : 0.0;
+    const double wi = i < n ? w * est[i] : 0.0;
+    const std::uint32_t cnt = n - b < 32 ? n - b : 32;
+    for (std::uint32_t l = 0; l < cnt; ++l) {
+      const double wl = __shfl_sync(0xffffffffu, w, l), wil = __shfl_sync(0xffffffffu, wi, l);
+      sum_w += wl;
+      sum_wi += wil;
+    }
+  }
+  mean = sum_wi / sum_w;
+  double chi2 = 0.0;
+  for (std::uint32_t b = 0; b < n; b += 32) {
+    const std::uint32_t i = b + lane;
+    double q = 0.0;
+    if (i < n) {
+      const double d = est[i] - mean;
+      q = d * d / var[i];
+    }
+    const std::uint32_t cnt = n - b < 32 ? n - b : 32;
+    for (std::uint32_t l = 0; l < cnt; ++l) chi2 += __shfl_sync(0xffffffffu, q, l);
+  }
+  const double dof = static_cast<double>(n > 1 ? n - 1 : 1);
+  sigma = 1.0 / sqrt(sum_w);
+  chi2_dof = chi2 / dof;
+}
+#endif
+
 /// weighted_estimate (driver.hpp:146-169) -- IEEE ops in the reference's order.
 MCB_HD void weighted_estimate_dev(const double* est, const double* var, std::uint32_t n, double& mean,
                                   double& sigma, double& chi2_dof) {
@@ -277,13 +355,14 @@ MCB_HD bool converged_dev(double est, double sigma, double chi2, double tau, dou
 
 // ------------------------------------------------------------------ finish (K3b + K4)
 struct RoundArgs {
-  const unsigned long long* words;  ///< [exchange_accs][kXWords]
+  unsigned long long* words;  ///< [exchange_accs][kXWords]; zeroed by the epilogue when zero_words
   std::uint32_t dims, nb, bin_axes;
   double md2;        ///< double(m) * double(m)  (sampler.hpp:330-331)
   double* est;       ///< 1 double
   double* var;       ///< 1 double
   double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
   const int* stop;
+  int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K3a (integrate loop)
 };
 
 struct EpilogueArgs {
@@ -301,6 +380,8 @@ struct EpilogueArgs {
 
 inline constexpr int kFinishThreads = 512;
 
+
+
 /// Phase 1 (all blocks): one warp per output value -- warp-cooperative exact
 /// rounding of the contributions, the estimate and the variance.
 /// Phase 2 (integrate only, the LAST block to finish phase 1): failure check,
@@ -312,6 +393,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
                                                                 int with_epilogue, unsigned int* counter) {
   extern __shared__ double fin_smem[];
   __shared__ bool is_last;
+  if (blockIdx.x == 0 && threadIdx.x == 0) MCB_FIN_STAMP(0);
   const int stop0 = r.stop ? *r.stop : 0;
   __syncthreads();  // every thread reads `stop` before the last block may set it
   if (stop0) return;
@@ -338,11 +420,13 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   if (!with_epilogue) return;
   __threadfence();
   __syncthreads();
+  if (threadIdx.x == 0) MCB_FIN_STAMP_MAX(1);
   if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
   if (threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) MCB_FIN_STAMP(2);
 
   double* contrib_s = fin_smem;
   double* scratch = fin_smem + static_cast<std::size_t>(r.dims) * r.nb;
@@ -360,10 +444,21 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
     }
     return;
   }
+  if (threadIdx.x == 0) MCB_FIN_STAMP(3);
+  // every block has read its words: ready the buffer for the next K3a, on the
+  // warps the adaptation leaves idle (all threads afterwards if none is idle)
+  const int nzero = (kScalarAccs + nbins) * kXWords;
+  const int busy = 32 * (e.adjusting ? e.adj_warps : 1);
+  if (r.zero_words && busy < static_cast<int>(blockDim.x) && static_cast<int>(threadIdx.x) >= busy)
+    for (int i = threadIdx.x - busy; i < nzero; i += blockDim.x - busy) r.words[i] = 0ull;
   if (e.adjusting) adjust_grid_block(e.adj, contrib_s, scratch, e.adj_warps);
-  if (threadIdx.x == 0) {
+  if (r.zero_words && busy >= static_cast<int>(blockDim.x))
+    for (int i = threadIdx.x; i < nzero; i += blockDim.x) r.words[i] = 0ull;
+  if (threadIdx.x == 0) MCB_FIN_STAMP(4);
+  if (threadIdx.x < 32) {
     double mean, sigma, chi2;
-    weighted_estimate_dev(e.hist_est, e.hist_var, e.it, mean, sigma, chi2);
+    weighted_estimate_warp(e.hist_est, e.hist_var, e.it, mean, sigma, chi2);
+    if (threadIdx.x != 0) return;
     st->estimate = mean;
     st->sigma = sigma;
     st->chi2_dof = chi2;
@@ -373,6 +468,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
       st->stop = 1;
     }
     if (e.host_flags) e.host_flags[e.it - 1] = st->stop ? 2 : 1;
+    MCB_FIN_STAMP(5);
   }
 }
 

@@ -607,6 +607,7 @@ class Run {
     MCB_CUDA(cudaMemsetAsync(ctx_.state.ensure(1), 0, sizeof(RunState), ctx_.stream()));
     MCB_CUDA(cudaMemsetAsync(ctx_.err_key.ensure(1), 0xff, sizeof(unsigned long long), ctx_.stream()));
     words_ = ctx_.words.ensure(exchange_words(cfg_.dims));
+    zero_exchange();
   }
 
   const SetupParams& params() const { return sp_; }
@@ -624,11 +625,20 @@ class Run {
     return static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
   }
   unsigned long long* exchange() const { return words_; }
+  void zero_exchange() {
+    MCB_CUDA(cudaMemsetAsync(words_, 0, sizeof(unsigned long long) * exchange_words(cfg_.dims), ctx_.stream()));
+    words_clean_ = true;
+  }
   /// Have finish() report per-iteration progress into host-mapped flags
   /// (Context::host_flags layout); nullptr turns it off.
   void set_host_flags(int* f) { host_flags_ = f; }
   /// Use a caller-owned exchange buffer (e.g. a torch tensor the caller all-reduces).
-  void set_exchange(unsigned long long* p) { words_ = p ? p : ctx_.words.get(); }
+  /// Use a caller-owned exchange buffer (it is zeroed here; finish() leaves it
+  /// zeroed for the next iteration's reduce()).
+  void set_exchange(unsigned long long* p) {
+    words_ = p ? p : ctx_.words.get();
+    zero_exchange();
+  }
   const int* stop_flag() const { return &ctx_.state.get()->stop; }
 
   /// K1 over the work slice [n0, n1) of the linear work index (default: all cubes).
@@ -641,7 +651,9 @@ class Run {
   /// K3a: this device's per-block partials -> exchange words.
   void reduce(std::uint32_t it) {
     if (it != last_it_) throw std::invalid_argument("reduce: iteration was not sampled");
-    launch_reduce(ctx_, last_, bin_axes(it), sh_.nb, words_, stop_flag());
+    // overwrite semantics; the memset is skipped when finish() left the words zeroed
+    launch_reduce(ctx_, last_, bin_axes(it), sh_.nb, words_, stop_flag(), words_clean_);
+    words_clean_ = false;
   }
 
   /// K3b + K4 (one fused kernel) for iteration it, after the optional
@@ -664,7 +676,8 @@ class Run {
                        ctx_.contrib.get()};
     e.host_flags = host_flags_;
     launch_finish(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
-                  ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e);
+                  ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e, /*zero_words=*/true);
+    words_clean_ = true;  // (or the run is stopped, and reduce() is a no-op)
   }
 
   RunState state() {
@@ -728,6 +741,7 @@ class Run {
   Launch last_{};
   std::uint32_t last_it_ = 0;
   int* host_flags_ = nullptr;
+  bool words_clean_ = false;  ///< exchange words are zero in stream order
 };
 
 /// integrate() for type-erased integrands: the whole schedule is enqueued

@@ -1,0 +1,70 @@
+// Per-phase device time of one small-ncall iteration (BASELINE C1: 5D f4,
+// 1e6 calls) through gpu::Run, CUDA events between the phases.
+//   ./latbench [rng 0|1] [maxcalls] [dims]
+#include <cstdio>
+#include <cstdlib>
+
+#include "mcubes_b200/mcubes.cuh"
+
+using namespace mcubes;
+
+int main(int argc, char** argv) {
+  const int rngk = argc > 1 ? std::atoi(argv[1]) : 1;
+  const std::uint64_t maxcalls = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1000000ull;
+  const int D = argc > 3 ? std::atoi(argv[3]) : 5;
+  RunConfig cfg;
+  cfg.dims = D;
+  cfg.maxcalls = maxcalls;
+  cfg.lower.assign(D, 0.0);
+  cfg.upper.assign(D, 1.0);
+  cfg.itmax = 40;
+  cfg.ita = 40;
+  cfg.tau_rel = 1e-15;
+  gpu::Context ctx(0);
+  const gpu::fn::F4 f{};
+  const gpu::IntegrandOps ops = rngk ? gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox>(f)
+                                     : gpu::make_ops<gpu::fn::F4, gpu::RngKind::compat>(f);
+  gpu::Run run(ctx, ops, cfg);
+  cudaEvent_t ev[4];
+  for (auto& e : ev) cudaEventCreate(&e);
+  double t[3] = {0, 0, 0};
+  int n = 0;
+  for (int it = 1; it <= 40; ++it) {
+    cudaEventRecord(ev[0], ctx.stream());
+    run.sample(it);
+    cudaEventRecord(ev[1], ctx.stream());
+    run.reduce(it);
+    cudaEventRecord(ev[2], ctx.stream());
+    run.finish(it);
+    cudaEventRecord(ev[3], ctx.stream());
+    cudaEventSynchronize(ev[3]);
+#ifdef MCB_FINISH_TIMING
+    if (it == 20) {
+      unsigned long long tt[16];
+      cudaMemcpyFromSymbol(tt, gpu::g_fin_times, sizeof tt);
+      std::printf("finish phases (us from start): blocks done %.2f  last block in %.2f  staged %.2f  adjusted %.2f  end %.2f\n",
+                  (tt[1] - tt[0]) * 1e-3, (tt[2] - tt[0]) * 1e-3, (tt[3] - tt[0]) * 1e-3, (tt[4] - tt[0]) * 1e-3,
+                  (tt[5] - tt[0]) * 1e-3);
+      std::printf("adjust axis 0 (us from start): loaded %.2f total %.2f imp %.2f sums %.2f walk %.2f check %.2f stored %.2f\n",
+                  (tt[8] - tt[0]) * 1e-3, (tt[9] - tt[0]) * 1e-3, (tt[10] - tt[0]) * 1e-3, (tt[11] - tt[0]) * 1e-3,
+                  (tt[12] - tt[0]) * 1e-3, (tt[13] - tt[0]) * 1e-3, (tt[14] - tt[0]) * 1e-3);
+    }
+    {
+      unsigned long long z[16] = {};
+      cudaMemcpyToSymbol(gpu::g_fin_times, z, sizeof z);
+    }
+#endif
+    if (it > 10) {
+      for (int k = 0; k < 3; ++k) {
+        float ms;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        t[k] += ms;
+      }
+      ++n;
+    }
+  }
+  std::printf("rng=%d D=%d maxcalls=%llu m=%llu p=%llu  per iteration (us): sample %.1f  reduce %.1f  finish %.1f\n",
+              rngk, D, (unsigned long long)maxcalls, (unsigned long long)run.params().m,
+              (unsigned long long)run.params().p, 1e3 * t[0] / n, 1e3 * t[1] / n, 1e3 * t[2] / n);
+  return 0;
+}
