@@ -3,6 +3,10 @@
 // K1-WS: the Philox-path sampling kernel with warp-specialised exact bin
 // deposits (adjusting iterations, all axes).
 //
+//
+// ARCHIVED EXPERIMENT (not built): measured slower than the single-role K1
+// because the shared-memory atomic unit, not latency, bounds the deposits
+// (DESIGN.md section 4).  Compile with -I include/mcubes_b200.
 // In K1 every warp alternates a compute phase (Philox, transform, integrand)
 // and a deposit phase whose three dependent shared-memory atomic rounds per
 // axis (carries travel through the returned old words, exact.cuh) leave the
