@@ -381,6 +381,10 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline()
         line["time_to_epsrel"] = time_to_epsrel(M, ctx)
+    elif world > 1 and not args.no_cpu:
+        tte = time_to_epsrel_dist(M, ctx, dist, dev, rank)
+        if rank == 0:
+            line["time_to_epsrel"] = tte
     if rank == 0:
         print(json.dumps(line), flush=True)
     run.close()
@@ -426,6 +430,42 @@ def time_to_epsrel(M, ctx):
         out.update(cpu_ms=1e3 * (time.perf_counter() - t0), cpu_iterations=o["iterations_used"],
                    cpu_converged=o["converged"], cpu_estimate=o["estimate"], cpu_sigma=o["sigma"],
                    cpu_threads=threads)
+    return out
+
+
+def time_to_epsrel_dist(M, ctx, dist, dev, rank):
+    """time_to_epsrel at N GPUs: paper_2202_01753_b200.dist.integrate (cube
+    ranges per rank, exact all-reduce per iteration), wall time max over ranks;
+    the reference CPU integrate is timed on rank 0's host cores."""
+    import torch
+
+    import oracle as O
+    from paper_2202_01753_b200 import dist as mdist
+
+    d, maxcalls, tau = 8, 10 ** 7, 1e-3
+    cfg = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
+                      upper=[1.0] * d)
+    f = M.make_suite_integrand(5, d)
+    mdist.integrate(f, cfg, ctx=ctx)  # warm
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    r = mdist.integrate(f, cfg, ctx=ctx)
+    ms = 1e3 * (time.perf_counter() - t0)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out = {"integrand": "f5", "dims": d, "maxcalls": maxcalls, "tau_rel": tau, "itmax": 30, "ita": 10, "seed": 1,
+           "gpu_ms": float(t.item()), "gpu_iterations": r.iterations_used, "gpu_converged": r.converged,
+           "gpu_estimate": r.estimate, "gpu_sigma": r.sigma, "path": "dist.integrate over all ranks"}
+    if rank == 0 and O.ref_available():
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        o = O.integrate("ref", 5, None, d, 50, maxcalls, 30, 10, tau, 1.5, 1.5, 1, 0, [0.0] * d, [1.0] * d,
+                        workers=threads)
+        out.update(cpu_ms=1e3 * (time.perf_counter() - t0), cpu_iterations=o["iterations_used"],
+                   cpu_converged=o["converged"], cpu_estimate=o["estimate"], cpu_sigma=o["sigma"],
+                   cpu_threads=threads)
+    dist.barrier()
     return out
 
 

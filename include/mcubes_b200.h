@@ -191,6 +191,13 @@ int mcb_run_destroy(mcb_run* run);
 uint64_t mcb_run_exchange_words(const mcb_run* run, uint32_t it);
 /* Use a caller-owned DEVICE buffer (>= max exchange words) for the exchange. */
 int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
+/* Progress reporting for early exit without a synchronising read: after
+ * iteration it has finished on the device, host_flags[it-1] = 1 (continue) or
+ * 2 (the run stopped: converged, failed or done).  host_flags must be pinned,
+ * device-accessible host memory of itmax ints, zeroed by the caller; NULL
+ * turns reporting off.  (No reference counterpart: the reference's integrate
+ * loop is synchronous, driver.hpp:227-256.) */
+int mcb_run_set_progress(mcb_run* run, int* host_flags);
 void* mcb_run_exchange_ptr(const mcb_run* run);
 /* Total linear work items (= m cubes). */
 uint64_t mcb_run_work_items(const mcb_run* run);

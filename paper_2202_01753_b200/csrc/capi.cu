@@ -346,6 +346,12 @@ int mcb_run_set_exchange(mcb_run* r, void* p) {
 
 void* mcb_run_exchange_ptr(const mcb_run* r) { return r ? r->run->exchange() : nullptr; }
 
+int mcb_run_set_progress(mcb_run* r, int* host_flags) {
+  if (!r) return MCB_EINVAL;
+  r->run->set_host_flags(host_flags);
+  return MCB_OK;
+}
+
 uint64_t mcb_run_work_items(const mcb_run* r) { return r ? r->run->params().m : 0; }
 
 int mcb_run_sample(mcb_run* r, uint32_t it, uint64_t n0, uint64_t n1) {

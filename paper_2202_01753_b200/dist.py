@@ -41,16 +41,29 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
         stream = torch.cuda.Stream(dev)
     ctx = ctx or M.Context(dev.index)
     ctx.set_stream(stream.cuda_stream)
+    # Bounded lookahead (as the single-GPU integrate): at most `ahead`
+    # iterations in flight; stop enqueuing once the device reports the run
+    # stopped through host-mapped progress flags.  The flags are identical on
+    # every rank (the state is), so all ranks leave the loop together.
+    ahead = 2
+    flags = torch.zeros(cfg.itmax, dtype=torch.int32).pin_memory()
+    events = [torch.cuda.Event() for _ in range(ahead + 1)]
     with torch.cuda.stream(stream):
         run = M.Run(f, cfg, ctx)
+        run.set_progress(flags.data_ptr())
         n0, n1 = partition(run.work_items, world, rank)
         xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
         run.set_exchange(xbuf.data_ptr())
         for it in range(1, cfg.itmax + 1):
+            if observer is None and it > ahead:
+                events[(it - ahead) % (ahead + 1)].synchronize()
+                if int(flags[it - ahead - 1]) != 1:
+                    break
             run.sample(it, n0, n1)
             run.reduce(it)
             dist.all_reduce(xbuf, group=group)  # exact integer sum across ranks
             run.finish(it)
+            events[it % (ahead + 1)].record(stream)
             if observer is not None:
                 r = run.result()
                 if r.iterations_used < it:

@@ -773,6 +773,10 @@ class Run:
     def set_exchange(self, device_ptr: int):
         _raise(self._lib.mcb_run_set_exchange(self.ptr, C.c_void_p(device_ptr)), self.ctx.ptr)
 
+    def set_progress(self, host_ptr: int):
+        """Host-mapped progress flags (mcb_run_set_progress): pinned int32[itmax], zeroed."""
+        _raise(self._lib.mcb_run_set_progress(self.ptr, C.c_void_p(host_ptr)), self.ctx.ptr)
+
     def sample(self, it: int, n0: int = 0, n1: int = (1 << 64) - 1):
         _raise(self._lib.mcb_run_sample(self.ptr, it, n0, n1), self.ctx.ptr, self.cfg.dims)
 

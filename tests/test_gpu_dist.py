@@ -18,9 +18,15 @@ pytestmark = pytest.mark.gpu
 D, MAXCALLS = 6, 2 * 10 ** 6
 
 
-def _cfg(M):
+def _cfg(M, early=False):
+    if early:  # converges at iteration 2 of 12: the ranks must leave the loop together
+        return M.RunConfig(dims=D, maxcalls=MAXCALLS, itmax=12, ita=6, tau_rel=2e-2, seed=13, lower=[0.0] * D,
+                           upper=[1.0] * D, rng="philox")
     return M.RunConfig(dims=D, maxcalls=MAXCALLS, itmax=6, ita=4, tau_rel=1e-15, seed=13, lower=[0.0] * D,
                        upper=[1.0] * D)
+
+
+FAMILY = {False: 4, True: 5}
 
 
 def _free_port():
@@ -31,7 +37,7 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, early):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -39,28 +45,31 @@ def _rank(rank, world, port, q):
         from paper_2202_01753_b200 import dist as mdist
 
         torch.cuda.set_device(0)
-        r = mdist.integrate(M.make_suite_integrand(4, D), _cfg(M))
+        r = mdist.integrate(M.make_suite_integrand(FAMILY[early], D), _cfg(M, early))
         q.put((rank, r.estimate, r.sigma, r.chi2_dof, [h.estimate for h in r.history],
-               [h.variance for h in r.history]))
+               [h.variance for h in r.history], r.converged, r.iterations_used))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_integrate_matches_single(world, ctx):
+@pytest.mark.parametrize("world,early", [(2, False), (3, False), (2, True)])
+def test_multi_rank_integrate_matches_single(world, early, ctx):
     import paper_2202_01753_b200 as M
 
-    want = M.integrate(M.make_suite_integrand(4, D), _cfg(M), ctx=ctx)
+    want = M.integrate(M.make_suite_integrand(FAMILY[early], D), _cfg(M, early), ctx=ctx)
+    if early:
+        assert want.converged and want.iterations_used < 12
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [mpc.Process(target=_rank, args=(r, world, port, q, early)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for _, est, sigma, chi2, he, hv in res:
+    for _, est, sigma, chi2, he, hv, conv, used in res:
+        assert conv == want.converged and used == want.iterations_used
         assert est == want.estimate and sigma == want.sigma and chi2 == want.chi2_dof
         assert he == [h.estimate for h in want.history] and hv == [h.variance for h in want.history]
