@@ -212,8 +212,8 @@ inline void set_round_keys(SampleArgs& a, std::uint64_t key) {
   for (int r = 0; r < 10; ++r) {
     a.round_keys[2 * r] = k0;
     a.round_keys[2 * r + 1] = k1;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
+    k0 += rng::kPhiloxW0;
+    k1 += rng::kPhiloxW1;
   }
 }
 

@@ -71,20 +71,6 @@ __device__ __noinline__ void carry_up(std::uint32_t* p, std::uint32_t* end) {
     if (atomicAdd(p, 1u) != 0xffffffffu) break;
 }
 
-/// Add pre-split digits at p = acc + dg.w (three word atomics, carries
-/// travel through the returned old values).  Branch-free except for the
-/// ~2^-11-probability ripple out of the top word.
-__device__ __forceinline__ void add_digits(std::uint32_t* p, std::uint32_t* end, const Digits& dg) {
-  const std::uint32_t o0 = atomicAdd(p, dg.d0);
-  const std::uint32_t c0 = (o0 + dg.d0) < o0 ? 1u : 0u;
-  const std::uint32_t t1 = dg.d1 + c0;  // wraps to 0 only if d1 == 0xffffffff and c0
-  const std::uint32_t o1 = atomicAdd(p + 1, t1);
-  const std::uint32_t c1 = ((t1 < c0) || ((o1 + t1) < o1)) ? 1u : 0u;
-  const std::uint32_t t2 = dg.d2 + c1;  // d2 < 2^21: never wraps
-  const std::uint32_t o2 = atomicAdd(p + 2, t2);
-  if ((o2 + t2) < o2) carry_up(p + 3, end);
-}
-
 /// Deposit the same digits into N accumulators (one per axis) -- the
 /// sampler's bin update, where every axis receives the same (f J)^2
 /// (sampler.hpp:173-176).  The atomics are issued word-major across the N
@@ -132,11 +118,7 @@ __device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::
 // loads and arithmetic around them.
 __device__ __forceinline__ std::uint32_t atoms_add(std::uint32_t addr, std::uint32_t v) {
   std::uint32_t old;
-#ifdef MCB_ATOMS_MEMCLOBBER
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-#else
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
-#endif
   return old;
 }
 
@@ -225,15 +207,6 @@ MCB_HD bool split_r24(double v, Digits2& out) {
 }
 
 #ifdef __CUDACC__
-/// Predicated shared atomic add (no-op, returns 0, when !on).
-__device__ __forceinline__ std::uint32_t atoms_add_if(std::uint32_t addr, std::uint32_t v, bool on) {
-  std::uint32_t old = 0;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.shared.add.u32 %0, [%1], %2;\n\t}"
-               : "+r"(old)
-               : "r"(addr), "r"(v), "r"(static_cast<std::uint32_t>(on)));
-  return old;
-}
-
 /// Deposit RN24 digits into N accumulators at shared-window addresses a[j]
 /// (= accumulator j + 4 dg.w): two word atomics (predicating the upper one
 /// off when its addend is zero measured slower), a rare ripple above.
@@ -249,11 +222,7 @@ __device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::
   std::uint32_t ripple = 0;
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-#ifdef MCB_PRED_UPPER
-    const std::uint32_t o = atoms_add_if(a[j] + 4, t1[j], t1[j] != 0);
-#else
     const std::uint32_t o = atoms_add(a[j] + 4, t1[j]);
-#endif
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t1[j]));
   }
   if (ripple) {
@@ -303,30 +272,6 @@ __device__ __forceinline__ void add_shared2(std::uint32_t* acc_a, double a, std:
   }
 }
 
-/// Add |v| exactly into a shared-memory accumulator of kXWords u32 words.
-/// Carries travel through the atomics' returned old values, so concurrent
-/// deposits from any lanes/warps compose to the exact total.
-__device__ __forceinline__ void add_shared(std::uint32_t* acc, double v) {
-  Digits dg;
-  if (!split(v, dg)) return;
-  std::uint32_t* p = acc + dg.w;
-  std::uint32_t o = atomicAdd(p, dg.d0);
-  std::uint32_t c = (o + dg.d0) < o;
-  const std::uint32_t t1 = dg.d1 + c;
-  c = t1 < c;  // d1 == 0xffffffff and a carry in
-  if (t1) {
-    o = atomicAdd(p + 1, t1);
-    c += (o + t1) < o;
-  }
-  const std::uint32_t t2 = dg.d2 + c;  // d2 < 2^21: never wraps
-  if (t2) {
-    o = atomicAdd(p + 2, t2);
-    if ((o + t2) < o) {
-      for (std::uint32_t k = dg.w + 3; k < static_cast<std::uint32_t>(kXWords); ++k)
-        if (atomicAdd(acc + k, 1u) != 0xffffffffu) break;
-    }
-  }
-}
 #endif
 
 /// Round the exact integer (pos - neg) * 2^-1074 to the nearest double, ties

@@ -136,8 +136,8 @@ __device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a
 __device__ __forceinline__ rng::U4 philox_rk(rng::U4 c, const std::uint32_t (&rk)[20]) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const std::uint64_t p0 = static_cast<std::uint64_t>(0xD2511F53u) * c.x;
-    const std::uint64_t p1 = static_cast<std::uint64_t>(0xCD9E8D57u) * c.z;
+    const std::uint64_t p0 = static_cast<std::uint64_t>(rng::kPhiloxM0) * c.x;
+    const std::uint64_t p1 = static_cast<std::uint64_t>(rng::kPhiloxM1) * c.z;
     c = rng::U4{static_cast<std::uint32_t>(p1 >> 32) ^ c.y ^ rk[2 * r], static_cast<std::uint32_t>(p1),
                 static_cast<std::uint32_t>(p0 >> 32) ^ c.w ^ rk[2 * r + 1], static_cast<std::uint32_t>(p0)};
   }
