@@ -139,6 +139,7 @@ class Context {
     if (own_stream_) cudaStreamDestroy(own_stream_);
     if (pinned_) cudaFreeHost(pinned_);
     if (flags_) cudaFreeHost(flags_);
+    if (staging_ev_) cudaEventDestroy(staging_ev_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
   }
   Context(const Context&) = delete;
@@ -166,6 +167,18 @@ class Context {
 
   static constexpr std::size_t kPinnedBytes = 1 << 20;
   unsigned char* pinned() const { return pinned_; }
+  /// Host writes into pinned() must not overtake asynchronous copies that
+  /// still read it: writers call staging_wait() first and staging_recorded()
+  /// after enqueuing their copies.
+  void staging_wait() {
+    if (staging_live_) MCB_CUDA(cudaEventSynchronize(staging_ev_));
+    staging_live_ = false;
+  }
+  void staging_recorded() {
+    if (!staging_ev_) MCB_CUDA(cudaEventCreateWithFlags(&staging_ev_, cudaEventDisableTiming));
+    MCB_CUDA(cudaEventRecord(staging_ev_, stream_));
+    staging_live_ = true;
+  }
 
   /// Host-mapped per-iteration progress flags written by the finish kernel
   /// (0 = not run, 1 = continue, 2 = stop), for integrate()'s bounded lookahead.
@@ -188,6 +201,8 @@ class Context {
   cudaStream_t own_stream_ = nullptr;
   cudaStream_t stream_ = nullptr;
   unsigned char* pinned_ = nullptr;
+  cudaEvent_t staging_ev_ = nullptr;
+  bool staging_live_ = false;
   int* flags_ = nullptr;
   std::vector<cudaEvent_t> events_;
 };

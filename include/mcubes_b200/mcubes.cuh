@@ -598,9 +598,25 @@ class Run {
     ctx_.activate();
     const Grid g0(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper);
     const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
-    upload(ctx_, ctx_.edges, g0.raw_edges().data(), n);
-    upload(ctx_, ctx_.lower, cfg_.lower.data(), cfg_.dims);
-    upload(ctx_, ctx_.upper, cfg_.upper.data(), cfg_.dims);
+    if (sizeof(double) * (n + 2 * cfg_.dims) <= Context::kPinnedBytes) {
+      // asynchronous copies from the pinned staging buffer (pageable sources
+      // would block the host for each)
+      ctx_.staging_wait();  // an earlier Run's copies may still read the buffer
+      auto* pin = reinterpret_cast<double*>(ctx_.pinned());
+      std::memcpy(pin, g0.raw_edges().data(), sizeof(double) * n);
+      std::memcpy(pin + n, cfg_.lower.data(), sizeof(double) * cfg_.dims);
+      std::memcpy(pin + n + cfg_.dims, cfg_.upper.data(), sizeof(double) * cfg_.dims);
+      MCB_CUDA(cudaMemcpyAsync(ctx_.edges.ensure(n), pin, sizeof(double) * n, cudaMemcpyHostToDevice, ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(ctx_.lower.ensure(cfg_.dims), pin + n, sizeof(double) * cfg_.dims,
+                               cudaMemcpyHostToDevice, ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(ctx_.upper.ensure(cfg_.dims), pin + n + cfg_.dims, sizeof(double) * cfg_.dims,
+                               cudaMemcpyHostToDevice, ctx_.stream()));
+      ctx_.staging_recorded();
+    } else {
+      upload(ctx_, ctx_.edges, g0.raw_edges().data(), n);
+      upload(ctx_, ctx_.lower, cfg_.lower.data(), cfg_.dims);
+      upload(ctx_, ctx_.upper, cfg_.upper.data(), cfg_.dims);
+    }
     ctx_.contrib.ensure(n);
     ctx_.hist_est.ensure(cfg_.itmax);
     ctx_.hist_var.ensure(cfg_.itmax);
@@ -702,22 +718,43 @@ class Run {
 
   /// Collect the result (one synchronisation); throws NonFiniteSample.
   IntegrationResult result() {
-    const RunState st = state();
+    // one synchronisation: state, error key and the whole history land in
+    // the context's pinned staging buffer together
+    unsigned char* pin = ctx_.pinned();
+    const std::size_t hbytes = sizeof(double) * cfg_.itmax;
+    const bool staged = sizeof(RunState) + 8 + 2 * hbytes <= Context::kPinnedBytes;
+    RunState st;
+    unsigned long long key = ~0ull;
+    std::vector<double> e, v;
+    if (staged) {
+      MCB_CUDA(cudaMemcpyAsync(pin, ctx_.state.get(), sizeof(RunState), cudaMemcpyDeviceToHost, ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState), ctx_.err_key.get(), 8, cudaMemcpyDeviceToHost, ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState) + 8, ctx_.hist_est.get(), hbytes, cudaMemcpyDeviceToHost,
+                               ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState) + 8 + hbytes, ctx_.hist_var.get(), hbytes,
+                               cudaMemcpyDeviceToHost, ctx_.stream()));
+      ctx_.sync();
+      std::memcpy(&st, pin, sizeof st);
+      std::memcpy(&key, pin + sizeof(RunState), 8);
+      const auto* he = reinterpret_cast<const double*>(pin + sizeof(RunState) + 8);
+      const auto* hv = reinterpret_cast<const double*>(pin + sizeof(RunState) + 8 + hbytes);
+      e.assign(he, he + st.iterations_used);
+      v.assign(hv, hv + st.iterations_used);
+    } else {
+      st = state();
+      MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
+      e.resize(st.iterations_used);
+      v.resize(st.iterations_used);
+      if (st.iterations_used) {
+        download(ctx_, e.data(), ctx_.hist_est.get(), st.iterations_used);
+        download(ctx_, v.data(), ctx_.hist_var.get(), st.iterations_used);
+      }
+      ctx_.sync();
+    }
     IntegrationResult res;
     res.params = sp_;
-    if (st.failed) {
-      unsigned long long key;
-      MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
-      ctx_.sync();
-      throw_nonfinite(ctx_, ops_, sh_, iteration_key(cfg_.seed, st.failed_iteration), key);
-    }
+    if (st.failed) throw_nonfinite(ctx_, ops_, sh_, iteration_key(cfg_.seed, st.failed_iteration), key);
     const std::uint32_t n = st.iterations_used;
-    std::vector<double> e(n), v(n);
-    if (n) {
-      download(ctx_, e.data(), ctx_.hist_est.get(), n);
-      download(ctx_, v.data(), ctx_.hist_var.get(), n);
-      ctx_.sync();
-    }
     for (std::uint32_t i = 0; i < n; ++i) {
       res.history.push_back({e[i], v[i], i + 1});
       res.total_samples += sp_.m * sp_.p;
