@@ -182,6 +182,15 @@ int mcb_grid_uniform(uint32_t dims, uint32_t n_bins, const double* lower, const 
 int mcb_integrate(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, mcb_result* result,
                   mcb_iteration* history, uint32_t history_cap, mcb_observer observer, void* user);
 
+/* ---- integrate() resumed from a checkpoint: `edges` (dims x n_bins) is the
+ * grid after the n_done completed iterations `done` (indices 1..n_done), e.g.
+ * read back with the grid.hpp:148-174 text format.  The stream is keyed by
+ * (seed, iteration), so the result is bitwise equal to the uninterrupted run.
+ * (The reference has the grid I/O but no resume entry point.) ---- */
+int mcb_integrate_resume(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, const double* edges,
+                         const mcb_iteration* done, uint32_t n_done, mcb_result* result, mcb_iteration* history,
+                         uint32_t history_cap, mcb_observer observer, void* user);
+
 /* ---- stepped run: the multi-GPU hook.  Each rank samples its slice of the
  * linear work index, the caller all-reduces (sum, uint64) the exchange buffer
  * across ranks, then every rank finishes the iteration identically. ---- */

@@ -626,6 +626,43 @@ class Run {
     zero_exchange();
   }
 
+  /// Resume from a checkpoint: the grid in force after `history.size()`
+  /// completed iterations and their results.  The stream is keyed by
+  /// (seed, iteration), so continuing at iteration history.size() + 1 gives
+  /// bit for bit the run that was never interrupted (grid.hpp:148-174 text
+  /// I/O carries the grid).  Returns that next iteration.
+  std::uint32_t resume(const Grid& grid, std::span<const IterationResult> history) {
+    if (grid.dims() != cfg_.dims || grid.n_bins() != cfg_.n_bins)
+      throw std::invalid_argument("resume: grid shape does not match the RunConfig");
+    for (std::uint32_t j = 0; j < cfg_.dims; ++j)
+      if (grid.lowers()[j] != cfg_.lower[j] || grid.uppers()[j] != cfg_.upper[j])
+        throw std::invalid_argument("resume: grid bounds do not match the RunConfig");
+    const std::uint32_t n = static_cast<std::uint32_t>(history.size());
+    if (n > cfg_.itmax) throw std::invalid_argument("resume: more completed iterations than itmax");
+    for (std::uint32_t i = 0; i < n; ++i)
+      if (history[i].index != i + 1) throw std::invalid_argument("resume: history indices must be 1..n");
+    upload(ctx_, ctx_.edges, grid.raw_edges().data(), std::size_t{cfg_.dims} * cfg_.n_bins);
+    RunState st{};
+    if (n) {
+      std::vector<double> e(n), v(n);
+      for (std::uint32_t i = 0; i < n; ++i) {
+        e[i] = history[i].estimate;
+        v[i] = history[i].variance;
+      }
+      upload(ctx_, ctx_.hist_est, e.data(), n);
+      upload(ctx_, ctx_.hist_var, v.data(), n);
+      const Combined c = weighted_estimate(history);  // driver.hpp:246-252, as the device epilogue does
+      st.iterations_used = n;
+      st.estimate = c.estimate;
+      st.sigma = c.sigma;
+      st.chi2_dof = c.chi2_dof;
+      if (check_convergence(c, cfg_)) st.converged = st.stop = 1;
+    }
+    MCB_CUDA(cudaMemcpyAsync(ctx_.state.get(), &st, sizeof st, cudaMemcpyHostToDevice, ctx_.stream()));
+    ctx_.sync();  // the host-side state copy above must land before it goes out of scope
+    return n + 1;
+  }
+
   const SetupParams& params() const { return sp_; }
   const Shape& shape() const { return sh_; }
   std::uint32_t bin_axes(std::uint32_t it) const {
@@ -784,8 +821,11 @@ class Run {
 /// integrate() for type-erased integrands: the whole schedule is enqueued
 /// without host synchronisation unless an observer wants per-iteration views.
 inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, const RunConfig& cfg,
-                                       const IterationObserver& observe = {}) {
+                                       const IterationObserver& observe = {}, const Grid* resume_grid = nullptr,
+                                       std::span<const IterationResult> resume_history = {}) {
   Run run(ctx, ops, cfg);
+  const std::uint32_t first = resume_grid ? run.resume(*resume_grid, resume_history) : 1u;
+  if (first > 1 && run.state().stop) return run.result();  // the checkpoint had already converged
   // Bounded lookahead: keep at most kAhead iterations in flight and stop
   // enqueuing once the finish kernel has reported convergence through the
   // host-mapped flags, so a run that converges early does not pay for the
@@ -798,8 +838,8 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
     std::memset(flags, 0, sizeof(int) * cfg.itmax);
     run.set_host_flags(flags);
   }
-  for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
-    if (lookahead && it > kAhead) {
+  for (std::uint32_t it = first; it <= cfg.itmax; ++it) {
+    if (lookahead && it >= first + kAhead) {
       const std::uint32_t back = it - kAhead;
       MCB_CUDA(cudaEventSynchronize(ctx.event(back % (kAhead + 1))));
       if (reinterpret_cast<volatile int*>(flags)[back - 1] != 1) break;  // stopped (or never ran: stopped earlier)
@@ -822,6 +862,18 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
 }
 
 }  // namespace gpu
+
+/// integrate() continued from a checkpoint (Run::resume): `grid` is the grid
+/// after the completed iterations `history` (1..n).  Bitwise equal to the
+/// uninterrupted run.
+template <gpu::DeviceIntegrand F>
+IntegrationResult integrate_resume(const F& f, const RunConfig& cfg, const Grid& grid,
+                                   std::span<const IterationResult> history, const IterationObserver& observe = {}) {
+  gpu::Context& ctx = gpu::default_context();
+  if (cfg.rng == gpu::RngKind::philox)
+    return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::philox>(f), cfg, observe, &grid, history);
+  return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::compat>(f), cfg, observe, &grid, history);
+}
 
 /// The full integration loop (driver.hpp:215-258), on the GPU.
 template <gpu::DeviceIntegrand F>

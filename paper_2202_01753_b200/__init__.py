@@ -8,6 +8,7 @@ library: the same API (``integrate``, ``v_sample``, ``v_sample_no_adjust``,
 from .mcubes import (  # noqa: F401
     BinAccumulator,
     BinUpdate,
+    Checkpoint,
     Combined,
     Context,
     CudaError,

@@ -79,6 +79,9 @@ SIGNATURES = {
     "mcb_grid_uniform": (C.c_int, [_U32, _U32, _PD, _PD, _PD]),
     "mcb_integrate": (C.c_int, [_VP, C.POINTER(mcb_integrand), C.POINTER(mcb_config),
                                 C.POINTER(mcb_result), C.POINTER(mcb_iteration), _U32, OBSERVER, _VP]),
+    "mcb_integrate_resume": (C.c_int, [_VP, C.POINTER(mcb_integrand), C.POINTER(mcb_config), _PD,
+                                       C.POINTER(mcb_iteration), _U32, C.POINTER(mcb_result),
+                                       C.POINTER(mcb_iteration), _U32, OBSERVER, _VP]),
     "mcb_run_create": (C.c_int, [_VP, C.POINTER(mcb_integrand), C.POINTER(mcb_config), C.POINTER(_VP)]),
     "mcb_run_destroy": (C.c_int, [_VP]),
     "mcb_run_exchange_words": (_U64, [_VP, _U32]),

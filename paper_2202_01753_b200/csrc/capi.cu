@@ -285,6 +285,12 @@ int mcb_grid_uniform(uint32_t dims, uint32_t n_bins, const double* lower, const 
 
 int mcb_integrate(mcb_ctx* c, const mcb_integrand* f, const mcb_config* cfgp, mcb_result* result,
                   mcb_iteration* history, uint32_t cap, mcb_observer observer, void* user) {
+  return mcb_integrate_resume(c, f, cfgp, nullptr, nullptr, 0, result, history, cap, observer, user);
+}
+
+int mcb_integrate_resume(mcb_ctx* c, const mcb_integrand* f, const mcb_config* cfgp, const double* edges,
+                         const mcb_iteration* done, uint32_t n_done, mcb_result* result, mcb_iteration* history,
+                         uint32_t cap, mcb_observer observer, void* user) {
   if (!c) return MCB_EINVAL;
   return guarded(c, [&] {
     Context& ctx = *c->ctx;
@@ -306,8 +312,16 @@ int mcb_integrate(mcb_ctx* c, const mcb_integrand* f, const mcb_config* cfgp, mc
         cv.bin_writes = v.bin_writes;
         observer(&cv, user);
       };
-    const auto r = mcubes::gpu::integrate_ops(ctx, ops, cfg, obs);
-    fill_result(r, result, history, cap);
+    if (!edges) {
+      if (n_done) throw std::invalid_argument("resume: completed iterations need the grid they produced");
+      fill_result(mcubes::gpu::integrate_ops(ctx, ops, cfg, obs), result, history, cap);
+      return;
+    }
+    if (n_done && !done) throw std::invalid_argument("resume: null history");
+    const mcubes::Grid grid = host_grid(cfg.dims, cfg.n_bins, cfg.lower.data(), cfg.upper.data(), edges);
+    std::vector<mcubes::IterationResult> h(n_done);
+    for (std::uint32_t i = 0; i < n_done; ++i) h[i] = {done[i].estimate, done[i].variance, done[i].index};
+    fill_result(mcubes::gpu::integrate_ops(ctx, ops, cfg, obs, &grid, h), result, history, cap);
   });
 }
 

@@ -706,10 +706,39 @@ def _result(r: "L.mcb_result", hist) -> IntegrationResult:
                              r.total_samples, r.bin_writes, SetupParams(r.g, r.m, r.p, r.s), h)
 
 
+@dataclass
+class Checkpoint:
+    """Resumable state of an integrate() run: the grid in
+    force after the completed iterations and their results.  The stream is
+    keyed by (seed, iteration), so resuming reproduces the uninterrupted run
+    bit for bit.  Text form: the grid in grid.hpp:148-158's format, then one
+    'index estimate variance' line per completed iteration (%.17g)."""
+    grid: "Grid"
+    history: List[IterationResult]
+
+    def write(self) -> str:
+        lines = [self.grid.write().rstrip("\n"), str(len(self.history))]
+        lines += [f"{h.index} {_g17(h.estimate)} {_g17(h.variance)}" for h in self.history]
+        return "\n".join(lines) + "\n"
+
+    @staticmethod
+    def read(text: str) -> "Checkpoint":
+        rows = text.strip().split("\n")
+        dims = int(rows[0].split()[0])
+        grid = Grid.read("\n".join(rows[:1 + dims]))
+        n = int(rows[1 + dims])
+        hist = []
+        for line in rows[2 + dims:2 + dims + n]:
+            i, e, v = line.split()
+            hist.append(IterationResult(float(e), float(v), int(i)))
+        return Checkpoint(grid, hist)
+
+
 def integrate(f: IntegrandSpec, cfg: RunConfig, observer: Optional[Callable[[IterationView], None]] = None,
-              ctx: Optional[Context] = None) -> IntegrationResult:
+              ctx: Optional[Context] = None, resume: Optional[Checkpoint] = None) -> IntegrationResult:
     """The full loop (driver.hpp:215-258) on the GPU.  Without an observer the
-    whole schedule is enqueued with one synchronisation at the end."""
+    whole schedule is enqueued with one synchronisation at the end.  With
+    `resume`, the run continues after the checkpoint's iterations."""
     ctx = ctx or default_context()
     fs, keep = f._c()
     c, keep2 = cfg._c()
@@ -731,7 +760,15 @@ def integrate(f: IntegrandSpec, cfg: RunConfig, observer: Optional[Callable[[Ite
             except Exception as e:  # pragma: no cover - surfaced after the call
                 errors.append(e)
         cb = L.OBSERVER(_cb)
-    rc = L.lib().mcb_integrate(ctx.ptr, C.byref(fs), C.byref(c), C.byref(res), hist, cfg.itmax, cb, None)
+    if resume is None:
+        rc = L.lib().mcb_integrate(ctx.ptr, C.byref(fs), C.byref(c), C.byref(res), hist, cfg.itmax, cb, None)
+    else:
+        done = (L.mcb_iteration * max(len(resume.history), 1))()
+        for i, h in enumerate(resume.history):
+            done[i] = L.mcb_iteration(h.estimate, h.variance, h.index, 0)
+        edges = np.ascontiguousarray(resume.grid.raw_edges, dtype=np.float64)
+        rc = L.lib().mcb_integrate_resume(ctx.ptr, C.byref(fs), C.byref(c), _dptr(edges), done,
+                                          len(resume.history), C.byref(res), hist, cfg.itmax, cb, None)
     _raise(rc, ctx.ptr, cfg.dims)
     if errors:
         raise errors[0]

@@ -180,3 +180,36 @@ def test_convergence_behaviour_matches_reference_8d(golden, ctx):
     c = [x for x in golden["integrate"] if x["name"] == "f5_8d_1e6_tau"][0]
     r = M.integrate(spec_of(c), cfg_of(c), ctx=ctx)
     assert r.iterations_used == c["iterations_used"] and r.converged == c["converged"]
+
+
+@pytest.mark.parametrize("rng,stop_at", [("compat", 3), ("compat", 7), ("philox", 5)])
+def test_resume_from_checkpoint_is_bitwise_the_uninterrupted_run(ctx, rng, stop_at):
+    """Checkpoint (grid text + history) after `stop_at` iterations, resume:
+    the same bits as the run that was never interrupted, across the ita
+    boundary too (the RNG is keyed by iteration)."""
+    d = 5
+    f = M.make_suite_integrand(4, d)
+    kw = dict(dims=d, maxcalls=2 * 10 ** 5, itmax=10, ita=5, tau_rel=1e-12, seed=3, lower=[0.0] * d,
+              upper=[1.0] * d, rng=rng)
+    full = M.integrate(f, M.RunConfig(**kw), ctx=ctx)
+    grids = []
+    M.integrate(f, M.RunConfig(**kw), observer=lambda v: grids.append(v.grid), ctx=ctx)
+    part = M.integrate(f, M.RunConfig(**{**kw, "itmax": stop_at, "ita": min(5, stop_at)}), ctx=ctx)
+    assert [bits(h.estimate) for h in part.history] == [bits(h.estimate) for h in full.history[:stop_at]]
+    cp = M.Checkpoint.read(M.Checkpoint(grids[stop_at - 1], part.history).write())  # through the text form
+    res = M.integrate(f, M.RunConfig(**kw), ctx=ctx, resume=cp)
+    assert res.iterations_used == full.iterations_used
+    assert [bits(h.estimate) for h in res.history] == [bits(h.estimate) for h in full.history]
+    assert [bits(h.variance) for h in res.history] == [bits(h.variance) for h in full.history]
+    assert bits(res.estimate) == bits(full.estimate) and bits(res.sigma) == bits(full.sigma)
+    assert bits(res.chi2_dof) == bits(full.chi2_dof)
+
+
+def test_resume_of_a_converged_checkpoint_returns_it(ctx):
+    cfg = M.RunConfig(dims=3, maxcalls=100000, seed=7, lower=[0.0] * 3, upper=[1.0] * 3)
+    f = M.make_suite_integrand(2, 3)
+    grids = []
+    r = M.integrate(f, cfg, observer=lambda v: grids.append(v.grid), ctx=ctx)
+    assert r.converged and r.iterations_used == 2
+    again = M.integrate(f, cfg, ctx=ctx, resume=M.Checkpoint(grids[-1], r.history))
+    assert again.converged and again.iterations_used == 2 and bits(again.estimate) == bits(r.estimate)

@@ -202,3 +202,15 @@ def test_partition_covers_range():
             cuts = [partition(m, world, r) for r in range(world)]
             assert cuts[0][0] == 0 and cuts[-1][1] == m
             assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+
+
+def test_checkpoint_text_round_trip():
+    import paper_2202_01753_b200 as M
+
+    g = M.Grid(3, 5, [0.0, -1.0, 2.0], [1.0, 1.0, 4.5])
+    hist = [M.IterationResult(0.1 + i / 3.0, 1e-7 * (i + 1) / 7.0, i + 1) for i in range(4)]
+    cp = M.Checkpoint(g, hist)
+    back = M.Checkpoint.read(cp.write())
+    assert np.array_equal(back.grid.raw_edges.view(np.uint64), g.raw_edges.view(np.uint64))
+    assert back.grid.lowers == g.lowers and back.grid.uppers == g.uppers
+    assert [(h.estimate, h.variance, h.index) for h in back.history] == [(h.estimate, h.variance, h.index) for h in hist]
