@@ -207,6 +207,10 @@ int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
  * turns reporting off.  (No reference counterpart: the reference's integrate
  * loop is synchronous, driver.hpp:227-256.) */
 int mcb_run_set_progress(mcb_run* run, int* host_flags);
+/* Resume a stepped run from a checkpoint (see mcb_integrate_resume); on
+ * success *next_iteration is the first iteration to sample. */
+int mcb_run_resume(mcb_run* run, const double* edges, const mcb_iteration* done, uint32_t n_done,
+                   uint32_t* next_iteration);
 void* mcb_run_exchange_ptr(const mcb_run* run);
 /* Total linear work items (= m cubes). */
 uint64_t mcb_run_work_items(const mcb_run* run);

@@ -360,6 +360,19 @@ int mcb_run_set_exchange(mcb_run* r, void* p) {
 
 void* mcb_run_exchange_ptr(const mcb_run* r) { return r ? r->run->exchange() : nullptr; }
 
+int mcb_run_resume(mcb_run* r, const double* edges, const mcb_iteration* done, uint32_t n_done,
+                   uint32_t* next_iteration) {
+  if (!r || !edges || (n_done && !done)) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    r->owner->ctx->activate();
+    const mcubes::Grid grid = host_grid(r->cfg.dims, r->cfg.n_bins, r->cfg.lower.data(), r->cfg.upper.data(), edges);
+    std::vector<mcubes::IterationResult> h(n_done);
+    for (std::uint32_t i = 0; i < n_done; ++i) h[i] = {done[i].estimate, done[i].variance, done[i].index};
+    const std::uint32_t next = r->run->resume(grid, h);
+    if (next_iteration) *next_iteration = next;
+  });
+}
+
 int mcb_run_set_progress(mcb_run* r, int* host_flags) {
   if (!r) return MCB_EINVAL;
   r->run->set_host_flags(host_flags);

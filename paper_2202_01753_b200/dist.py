@@ -27,9 +27,10 @@ def partition(m: int, world: int, rank: int):
 
 
 def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.Context] = None,
-              observer=None) -> M.IntegrationResult:
+              observer=None, resume: Optional[M.Checkpoint] = None) -> M.IntegrationResult:
     """integrate() across the ranks of `group` (default: WORLD).  Every rank
-    returns the same IntegrationResult."""
+    returns the same IntegrationResult.  `resume` continues from a checkpoint
+    (every rank passes the same one)."""
     import torch
     import torch.distributed as dist
 
@@ -54,8 +55,13 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
         n0, n1 = partition(run.work_items, world, rank)
         xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
         run.set_exchange(xbuf.data_ptr())
-        for it in range(1, cfg.itmax + 1):
-            if observer is None and it > ahead:
+        first = run.resume(resume) if resume is not None else 1
+        if first > 1 and run.result().converged:
+            res = run.result()
+            run.close()
+            return res
+        for it in range(first, cfg.itmax + 1):
+            if observer is None and it >= first + ahead:
                 events[(it - ahead) % (ahead + 1)].synchronize()
                 if int(flags[it - ahead - 1]) != 1:
                     break

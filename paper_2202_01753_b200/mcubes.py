@@ -810,6 +810,16 @@ class Run:
     def set_exchange(self, device_ptr: int):
         _raise(self._lib.mcb_run_set_exchange(self.ptr, C.c_void_p(device_ptr)), self.ctx.ptr)
 
+    def resume(self, cp: "Checkpoint") -> int:
+        """Continue from a checkpoint (mcb_run_resume); returns the next iteration."""
+        done = (L.mcb_iteration * max(len(cp.history), 1))()
+        for i, h in enumerate(cp.history):
+            done[i] = L.mcb_iteration(h.estimate, h.variance, h.index, 0)
+        edges = np.ascontiguousarray(cp.grid.raw_edges, dtype=np.float64)
+        nxt = C.c_uint32()
+        _raise(self._lib.mcb_run_resume(self.ptr, _dptr(edges), done, len(cp.history), C.byref(nxt)), self.ctx.ptr)
+        return nxt.value
+
     def set_progress(self, host_ptr: int):
         """Host-mapped progress flags (mcb_run_set_progress): pinned int32[itmax], zeroed."""
         _raise(self._lib.mcb_run_set_progress(self.ptr, C.c_void_p(host_ptr)), self.ctx.ptr)

@@ -19,14 +19,23 @@ D, MAXCALLS = 6, 2 * 10 ** 6
 
 
 def _cfg(M, early=False):
-    if early:  # converges at iteration 2 of 12: the ranks must leave the loop together
+    if early is True:  # converges at iteration 2 of 12: the ranks must leave the loop together
         return M.RunConfig(dims=D, maxcalls=MAXCALLS, itmax=12, ita=6, tau_rel=2e-2, seed=13, lower=[0.0] * D,
                            upper=[1.0] * D, rng="philox")
     return M.RunConfig(dims=D, maxcalls=MAXCALLS, itmax=6, ita=4, tau_rel=1e-15, seed=13, lower=[0.0] * D,
                        upper=[1.0] * D)
 
 
-FAMILY = {False: 4, True: 5}
+FAMILY = {False: 4, True: 5, "resume": 4}
+
+
+def _checkpoint(M, k):
+    """Grid and history after k iterations of the uninterrupted single-process run."""
+    grids = []
+    cfg = _cfg(M)
+    part = M.integrate(M.make_suite_integrand(4, D), M.RunConfig(**{**cfg.__dict__, "itmax": k, "ita": min(k, cfg.ita)}),
+                       observer=lambda v: grids.append(v.grid))
+    return M.Checkpoint(grids[-1], part.history)
 
 
 def _free_port():
@@ -45,19 +54,20 @@ def _rank(rank, world, port, q, early):
         from paper_2202_01753_b200 import dist as mdist
 
         torch.cuda.set_device(0)
-        r = mdist.integrate(M.make_suite_integrand(FAMILY[early], D), _cfg(M, early))
+        resume = _checkpoint(M, 3) if early == "resume" else None
+        r = mdist.integrate(M.make_suite_integrand(FAMILY[early], D), _cfg(M, early), resume=resume)
         q.put((rank, r.estimate, r.sigma, r.chi2_dof, [h.estimate for h in r.history],
                [h.variance for h in r.history], r.converged, r.iterations_used))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,early", [(2, False), (3, False), (2, True)])
+@pytest.mark.parametrize("world,early", [(2, False), (3, False), (2, True), (2, "resume")])
 def test_multi_rank_integrate_matches_single(world, early, ctx):
     import paper_2202_01753_b200 as M
 
     want = M.integrate(M.make_suite_integrand(FAMILY[early], D), _cfg(M, early), ctx=ctx)
-    if early:
+    if early is True:
         assert want.converged and want.iterations_used < 12
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
