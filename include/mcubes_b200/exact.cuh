@@ -64,55 +64,9 @@ MCB_HD bool split(double v, Digits& out) {
 }
 
 #ifdef __CUDACC__
-/// Rare tail of a deposit: a carry out of the third word ripples upward.
-template <int kTag = 0>
-__device__ __noinline__ void carry_up(std::uint32_t* p, std::uint32_t* end) {
-  for (; p < end; ++p)
-    if (atomicAdd(p, 1u) != 0xffffffffu) break;
-}
-
-/// Deposit the same digits into N accumulators (one per axis) -- the
-/// sampler's bin update, where every axis receives the same (f J)^2
-/// (sampler.hpp:173-176).  The atomics are issued word-major across the N
-/// accumulators, so a sample pays three shared-memory round trips instead of
-/// 3N, and the rare ripple out of the top word is one check per sample.
-/// p[j] = accumulator j + dg.w.
-template <int N>
-__device__ __forceinline__ void add_digits_n(std::uint32_t* const (&p)[N], std::uint32_t* end, const Digits& dg) {
-  // Carry arithmetic in PTX add.cc/addc (SASS: IADD3 with predicate
-  // carry-out / IADD3.X carry-in): per word the carry out of (old + digit)
-  // is folded straight into the next word's addend.
-  std::uint32_t t1[N], u[N];
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const std::uint32_t o = atomicAdd(p[j], dg.d0);
-    // t1 = d1 + carry(o + d0); u = d2 + carry(t1 wrapped)   (d2 < 2^21: u never wraps)
-    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
-        : "=r"(t1[j]), "=r"(u[j])
-        : "r"(o), "r"(dg.d0), "r"(dg.d1), "r"(dg.d2));
-  }
-  std::uint32_t t2[N];
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const std::uint32_t o = atomicAdd(p[j] + 1, t1[j]);
-    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(t2[j]) : "r"(o), "r"(t1[j]), "r"(u[j]));
-  }
-  std::uint32_t ripple = 0;  // bit (N-1-j) = carry out of axis j's top word
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const std::uint32_t o = atomicAdd(p[j] + 2, t2[j]);
-    asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t2[j]));
-  }
-  if (ripple) {
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-      if ((ripple >> (N - 1 - j)) & 1u) carry_up(p[j] + 3, end);
-  }
-}
-
-// ---- the same deposits on 32-bit shared-window addresses (atom.shared):
-// no 64-bit generic-pointer arithmetic per axis, and constant per-axis row
-// offsets fold into the instruction's immediate.
+// ---- exact deposits on 32-bit shared-window addresses (atom.shared): no
+// 64-bit generic-pointer arithmetic per axis; constant per-axis row offsets
+// fold into the instruction's immediate.
 // No "memory" clobber: the accumulators are only read after __syncthreads(),
 // and atomics to distinct words commute, so the compiler may schedule other
 // loads and arithmetic around them.
@@ -122,13 +76,21 @@ __device__ __forceinline__ std::uint32_t atoms_add(std::uint32_t addr, std::uint
   return old;
 }
 
+/// Rare tail of a deposit: a carry out of the top word ripples upward.
 template <int kTag = 0>
 __device__ __noinline__ void carry_up_s(std::uint32_t addr, std::uint32_t end) {
   for (; addr < end; addr += 4)
     if (atoms_add(addr, 1u) != 0xffffffffu) break;
 }
 
-/// add_digits_n on shared-window byte addresses a[j] (= accumulator j + 4 dg.w).
+/// Deposit the same digits into N accumulators (one per axis) -- the
+/// sampler's bin update, where every axis receives the same (f J)^2
+/// (sampler.hpp:173-176) -- at shared-window byte addresses a[j]
+/// (= accumulator j + 4 dg.w).  The atomics are issued word-major across the N
+/// accumulators, so a sample pays three shared-memory round trips instead of
+/// 3N; carries travel through the returned old words (PTX add.cc/addc: IADD3
+/// with predicate carry-out / IADD3.X), and the rare ripple out of the top
+/// word is one check per sample.
 template <int N>
 __device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::uint32_t end, const Digits& dg) {
   std::uint32_t t1[N], u[N];
@@ -228,47 +190,47 @@ __device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::
   if (ripple) {
 #pragma unroll
     for (int j = 0; j < N; ++j)
-      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(a[j] + 8, end);
+      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a[j] + 8, 1u) == 0xffffffffu) carry_up_s(a[j] + 12, end);
   }
 }
 #endif
 
-/// Two independent exact adds (the per-cube estimate and variance), issued
-/// interleaved so their atomic round trips overlap.
-__device__ __forceinline__ void add_shared2(std::uint32_t* acc_a, double a, std::uint32_t* acc_b, double b,
-                                            std::uint32_t* end_a, std::uint32_t* end_b) {
+/// Two independent exact adds (the per-cube estimate and variance) at
+/// shared-window addresses a_s / b_s (accumulator bases), issued interleaved
+/// so their atomic round trips overlap.
+__device__ __forceinline__ void add_shared2_s(std::uint32_t a_s, double a, std::uint32_t b_s, double b,
+                                              std::uint32_t end_s) {
   Digits da, db;
   const bool ha = split(a, da), hb = split(b, db);
   if (ha && hb) {
-    std::uint32_t* const pa[1] = {acc_a + da.w};
-    std::uint32_t* const pb[1] = {acc_b + db.w};
+    const std::uint32_t pa = a_s + 4u * da.w, pb = b_s + 4u * db.w;
     // the two accumulators receive different digits: interleave by hand
     std::uint32_t ta, ua, tb, ub;
-    std::uint32_t o = atomicAdd(pa[0], da.d0);
+    std::uint32_t o = atoms_add(pa, da.d0);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
         : "=r"(ta), "=r"(ua) : "r"(o), "r"(da.d0), "r"(da.d1), "r"(da.d2));
-    o = atomicAdd(pb[0], db.d0);
+    o = atoms_add(pb, db.d0);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
         : "=r"(tb), "=r"(ub) : "r"(o), "r"(db.d0), "r"(db.d1), "r"(db.d2));
-    o = atomicAdd(pa[0] + 1, ta);
+    o = atoms_add(pa + 4, ta);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(ta) : "r"(o), "r"(ta), "r"(ua));
-    o = atomicAdd(pb[0] + 1, tb);
+    o = atoms_add(pb + 4, tb);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}" : "=r"(tb) : "r"(o), "r"(tb), "r"(ub));
     std::uint32_t ra = 0, rb = 0;
-    o = atomicAdd(pa[0] + 2, ta);
+    o = atoms_add(pa + 8, ta);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t}" : "=r"(ra) : "r"(o), "r"(ta));
-    o = atomicAdd(pb[0] + 2, tb);
+    o = atoms_add(pb + 8, tb);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t}" : "=r"(rb) : "r"(o), "r"(tb));
     if (ra | rb) {
-      if (ra) carry_up(pa[0] + 3, end_a);
-      if (rb) carry_up(pb[0] + 3, end_b);
+      if (ra) carry_up_s(pa + 12, end_s);
+      if (rb) carry_up_s(pb + 12, end_s);
     }
   } else if (ha) {
-    std::uint32_t* const pa[1] = {acc_a + da.w};
-    add_digits_n<1>(pa, end_a, da);
+    const std::uint32_t pa[1] = {a_s + 4u * da.w};
+    add_digits_s<1>(pa, end_s, da);
   } else if (hb) {
-    std::uint32_t* const pb[1] = {acc_b + db.w};
-    add_digits_n<1>(pb, end_b, db);
+    const std::uint32_t pb[1] = {b_s + 4u * db.w};
+    add_digits_s<1>(pb, end_s, db);
   }
 }
 

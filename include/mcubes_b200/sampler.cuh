@@ -351,14 +351,15 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   __syncthreads();
 
   const int lane = tid & 31;
-  std::uint32_t* est_pos = acc + (0 * kLaneCopies + lane) * kXWords;
-  std::uint32_t* est_neg = acc + (1 * kLaneCopies + lane) * kXWords;
-  std::uint32_t* var_acc = acc + (2 * kLaneCopies + lane) * kXWords;
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
-  std::uint32_t* const acc_end = acc + nacc * kXWords;
-  // 32-bit shared-window byte addresses of the bin accumulators
-  const std::uint32_t bins_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(bins));
-  const std::uint32_t end_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(acc_end));
+  // 32-bit shared-window byte addresses of the accumulators
+  const std::uint32_t acc_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(acc));
+  constexpr std::uint32_t kAccBytes = 4u * kXWords;
+  const std::uint32_t est_pos_s = acc_s + (0 * kLaneCopies + lane) * kAccBytes;
+  const std::uint32_t est_neg_s = acc_s + (1 * kLaneCopies + lane) * kAccBytes;
+  const std::uint32_t var_s = acc_s + (2 * kLaneCopies + lane) * kAccBytes;
+  const std::uint32_t bins_s = acc_s + kScalarAccs * kLaneCopies * kAccBytes;
+  const std::uint32_t end_s = acc_s + static_cast<std::uint32_t>(nacc) * kAccBytes;
   const std::uint32_t bin_axes = a.bin_axes;
   constexpr std::uint32_t kCell = 4u * kXWords;  // bytes per accumulator
 
@@ -454,8 +455,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       var = __dmul_rn(m2, a.rcp_pp1);
     }
     if (!(var > 0.0)) var = 0.0;
-    std::uint32_t* const est_acc = sum < 0.0 ? est_neg : est_pos;
-    exact::add_shared2(est_acc, sum, var_acc, var, est_acc + kXWords, var_acc + kXWords);
+    exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
 
     bool all_axes;
     active = cw.next(a, T, all_axes);
