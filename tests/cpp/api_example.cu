@@ -3,6 +3,7 @@
 // grid.hpp) compiles unchanged except for the include line and the
 // __host__ __device__ marker on the functor, and runs on the GPU.
 // Prints machine-readable lines checked by tests/test_gpu_cpp_api.py.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <span>
@@ -24,6 +25,16 @@ struct Bump {
 // (a CUDA rule); state travels by value.
 struct Seven {
   __host__ __device__ double operator()(std::span<const double>) const { return 7.0; }
+};
+// BASELINE config 3's optional variant: a sharply peaked normalised Gaussian,
+// sigma = 0.01 per axis, centred at 1/2 (a user functor, not a built-in).
+struct SharpGauss {
+  double inv2s2, norm;  // 1 / (2 sigma^2), (2 pi sigma^2)^(-d/2)
+  __host__ __device__ double operator()(std::span<const double> x) const {
+    double s = 0.0;
+    for (const double xi : x) s += (xi - 0.5) * (xi - 0.5);
+    return norm * std::exp(-s * inv2s2);
+  }
 };
 struct Bad {
   __host__ __device__ double operator()(std::span<const double> x) const { return x[0] > 0.5 ? INFINITY : 1.0; }
@@ -57,6 +68,43 @@ int main() {
     std::printf("NONFINITE none\n");
   } catch (const mcubes::NonFiniteSample& e) {
     std::printf("NONFINITE x0 %.17g value %g\n", e.point()[0], e.value());
+  }
+  // BASELINE config 3 (sigma 0.01 variant) on the Philox path: 6D at 1e9 calls per iteration
+  {
+    const double sg = 0.01;
+    mcubes::RunConfig c3;
+    c3.dims = 6;
+    c3.maxcalls = 1000000000ull;
+    c3.itmax = 4;
+    c3.ita = 3;
+    c3.tau_rel = 1e-12;
+    c3.lower.assign(6, 0.0);
+    c3.upper.assign(6, 1.0);
+    c3.rng = mcubes::gpu::RngKind::philox;
+    const SharpGauss fg{1.0 / (2.0 * sg * sg), std::pow(2.0 * M_PI * sg * sg, -3.0)};
+    (void)mcubes::integrate(fg, c3);  // warm-up (module load)
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto r3 = mcubes::integrate(fg, c3);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const double truth = std::pow(std::erf(0.5 / (sg * std::sqrt(2.0))), 6.0);
+    std::printf("C3SHARP estimate %.17g sigma %.17g truth %.17g iterations %u evals_per_s %.6g\n", r3.estimate, r3.sigma,
+                truth, r3.iterations_used, static_cast<double>(r3.total_samples) / secs);
+  }
+
+  // checkpoint / resume through the C++ API: 2 iterations, then the rest
+  {
+    mcubes::RunConfig rc = cfg;
+    rc.tau_rel = 1e-12;
+    rc.itmax = 6;
+    rc.ita = 4;
+    std::vector<mcubes::Grid> grids;
+    const auto full = mcubes::integrate(Bump{1.0 / 50.0}, rc, [&](const mcubes::IterationView& v) { grids.push_back(v.grid); });
+    mcubes::RunConfig first = rc;
+    first.itmax = 2;
+    first.ita = 2;
+    const auto part = mcubes::integrate(Bump{1.0 / 50.0}, first);
+    const auto res2 = mcubes::integrate_resume(Bump{1.0 / 50.0}, rc, grids[1], part.history);
+    std::printf("RESUME same %d\n", res2.estimate == full.estimate && res2.sigma == full.sigma ? 1 : 0);
   }
   return 0;
 }
