@@ -421,7 +421,16 @@ def time_to_epsrel(M, ctx):
     gpu_ms = 1e3 * (time.perf_counter() - t0)
     out = {"integrand": "f5", "dims": d, "maxcalls": maxcalls, "tau_rel": tau, "itmax": 30, "ita": 10, "seed": 1,
            "gpu_ms": gpu_ms, "gpu_iterations": r.iterations_used, "gpu_converged": r.converged,
-           "gpu_estimate": r.estimate, "gpu_sigma": r.sigma}
+           "gpu_estimate": r.estimate, "gpu_sigma": r.sigma, "gpu_rng": "compat (same estimate bits as the CPU)"}
+    # the same question on the Philox stream (its own convergence decision for this seed)
+    cfgp = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
+                       upper=[1.0] * d, rng="philox")
+    M.integrate(f, cfgp, ctx=ctx)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rp = M.integrate(f, cfgp, ctx=ctx)
+    out.update(philox_gpu_ms=1e3 * (time.perf_counter() - t0), philox_iterations=rp.iterations_used,
+               philox_converged=rp.converged, philox_estimate=rp.estimate, philox_sigma=rp.sigma)
     if O.ref_available():
         threads = os.cpu_count() or 1
         t0 = time.perf_counter()
