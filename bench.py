@@ -406,39 +406,54 @@ def cpu_baseline():
 
 def time_to_epsrel(M, ctx):
     """Time-to-target-relative-error (BASELINE metric, config 2) for 8D f5 at
-    tau_rel 1e-3: GPU integrate() vs the reference integrate() on host cores."""
+    tau_rel 1e-3: GPU integrate() (both streams) vs the reference integrate()
+    on host cores.  Seed 1 is reported in full (the compat stream reaches the
+    reference's estimate bit for bit); seeds 0..9 give medians, since whether
+    a given seed passes the chi^2 gate early is luck on any stream."""
     import oracle as O
     import torch
 
     d, maxcalls, tau = 8, 10 ** 7, 1e-3
-    cfg = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
-                      upper=[1.0] * d)
     f = M.make_suite_integrand(5, d)
-    M.integrate(f, cfg, ctx=ctx)  # warm
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    r = M.integrate(f, cfg, ctx=ctx)
-    gpu_ms = 1e3 * (time.perf_counter() - t0)
+
+    def cfg(seed, rng):
+        return M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=seed, lower=[0.0] * d,
+                           upper=[1.0] * d, rng=rng)
+
+    def gpu(seed, rng):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = M.integrate(f, cfg(seed, rng), ctx=ctx)
+        return r, 1e3 * (time.perf_counter() - t0)
+
+    M.integrate(f, cfg(1, "compat"), ctx=ctx)  # warm
+    M.integrate(f, cfg(1, "philox"), ctx=ctx)
+    r, gpu_ms = gpu(1, "compat")
     out = {"integrand": "f5", "dims": d, "maxcalls": maxcalls, "tau_rel": tau, "itmax": 30, "ita": 10, "seed": 1,
            "gpu_ms": gpu_ms, "gpu_iterations": r.iterations_used, "gpu_converged": r.converged,
            "gpu_estimate": r.estimate, "gpu_sigma": r.sigma, "gpu_rng": "compat (same estimate bits as the CPU)"}
-    # the same question on the Philox stream (its own convergence decision for this seed)
-    cfgp = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
-                       upper=[1.0] * d, rng="philox")
-    M.integrate(f, cfgp, ctx=ctx)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rp = M.integrate(f, cfgp, ctx=ctx)
-    out.update(philox_gpu_ms=1e3 * (time.perf_counter() - t0), philox_iterations=rp.iterations_used,
-               philox_converged=rp.converged, philox_estimate=rp.estimate, philox_sigma=rp.sigma)
+    seeds = range(10)
+    runs = {rng: [gpu(s, rng) for s in seeds] for rng in ("compat", "philox")}
+    for rng, rr in runs.items():
+        out[f"median10_{rng}_gpu_ms"] = statistics.median(ms for _, ms in rr)
+        out[f"median10_{rng}_iterations"] = statistics.median(x.iterations_used for x, _ in rr)
+        out[f"converged10_{rng}"] = sum(x.converged for x, _ in rr)
     if O.ref_available():
         threads = os.cpu_count() or 1
-        t0 = time.perf_counter()
-        o = O.integrate("ref", 5, None, d, 50, maxcalls, 30, 10, tau, 1.5, 1.5, 1, 0, [0.0] * d, [1.0] * d,
-                        workers=threads)
-        out.update(cpu_ms=1e3 * (time.perf_counter() - t0), cpu_iterations=o["iterations_used"],
-                   cpu_converged=o["converged"], cpu_estimate=o["estimate"], cpu_sigma=o["sigma"],
-                   cpu_threads=threads)
+
+        def cpu(seed):
+            t0 = time.perf_counter()
+            o = O.integrate("ref", 5, None, d, 50, maxcalls, 30, 10, tau, 1.5, 1.5, seed, 0, [0.0] * d, [1.0] * d,
+                            workers=threads)
+            return o, 1e3 * (time.perf_counter() - t0)
+
+        o, cms = cpu(1)
+        out.update(cpu_ms=cms, cpu_iterations=o["iterations_used"], cpu_converged=o["converged"],
+                   cpu_estimate=o["estimate"], cpu_sigma=o["sigma"], cpu_threads=threads)
+        cr = [cpu(s) for s in seeds]
+        out["median10_cpu_ms"] = statistics.median(ms for _, ms in cr)
+        out["median10_cpu_iterations"] = statistics.median(x["iterations_used"] for x, _ in cr)
+        out["converged10_cpu"] = sum(x["converged"] for x, _ in cr)
     return out
 
 
