@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <utility>
 
 #include "config.cuh"
 
@@ -191,6 +192,48 @@ __device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::
 #pragma unroll
     for (int j = 0; j < N; ++j)
       if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a[j] + 8, 1u) == 0xffffffffu) carry_up_s(a[j] + 12, end);
+  }
+}
+#endif
+
+#ifdef __CUDACC__
+/// atom.shared.add at a register address plus a compile-time byte offset
+/// (folded into the instruction: [R + imm]).
+template <std::uint32_t Off>
+__device__ __forceinline__ std::uint32_t atoms_add_at(std::uint32_t addr, std::uint32_t v) {
+  std::uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1+%2], %3;" : "=r"(old) : "r"(addr), "n"(Off), "r"(v));
+  return old;
+}
+
+/// add_digits2_s for the N axes of one sample when the axis stride kRow is a
+/// compile-time constant: base[j] = word-w address of bin[j] in axis 0's row;
+/// axis j's row offset j*kRow rides in the atomics' immediates, so a deposit
+/// costs one IMAD of address arithmetic per axis.
+template <int N, std::uint32_t kRow>
+__device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N], std::uint32_t end,
+                                                 const Digits2& dg) {
+  std::uint32_t t1[N];
+  [&]<std::size_t... J>(std::index_sequence<J...>) {
+    ((void)[&] {
+      const std::uint32_t o = atoms_add_at<static_cast<std::uint32_t>(J) * kRow>(base[J], dg.d0);
+      asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}"
+          : "=r"(t1[J]) : "r"(o), "r"(dg.d0), "r"(dg.d1));
+    }(), ...);
+  }(std::make_index_sequence<N>{});
+  std::uint32_t ripple = 0;
+  [&]<std::size_t... J>(std::index_sequence<J...>) {
+    ((void)[&] {
+      const std::uint32_t o = atoms_add_at<static_cast<std::uint32_t>(J) * kRow + 4u>(base[J], t1[J]);
+      asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t1[J]));
+    }(), ...);
+  }(std::make_index_sequence<N>{});
+  if (ripple) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const std::uint32_t a = base[j] + static_cast<std::uint32_t>(j) * kRow;
+      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a + 8, 1u) == 0xffffffffu) carry_up_s(a + 12, end);
+    }
   }
 }
 #endif

@@ -376,11 +376,18 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     if (nz) {
       const std::uint32_t wb = bins_s + 4u * dgt.w;
       if (bin_axes == static_cast<std::uint32_t>(D)) {
-        std::uint32_t ad[D];
+        if constexpr (R == RngKind::philox && NB != 0) {  // row offsets as immediates
+          std::uint32_t base[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
-        if constexpr (R == RngKind::compat) exact::add_digits_s<D>(ad, end_s, dgt);
-        else exact::add_digits2_s<D>(ad, end_s, dgt);
+          for (int j = 0; j < D; ++j) base[j] = wb + bin[j] * kCell;
+          exact::add_digits2_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
+        } else {
+          std::uint32_t ad[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
+          if constexpr (R == RngKind::compat) exact::add_digits_s<D>(ad, end_s, dgt);
+          else exact::add_digits2_s<D>(ad, end_s, dgt);
+        }
       } else {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
         if constexpr (R == RngKind::compat) exact::add_digits_s<1>(ad, end_s, dgt);
