@@ -1,8 +1,9 @@
 // SPDX-License-Identifier: Apache-2.0
 //
 // Host engine: device context, buffers and the launch sequence of one m-Cubes
-// iteration (K1 sample -> K3a exact cross-block sum -> [all-reduce] -> K3b
-// round -> K4 adapt/combine).  Everything here is stream-ordered; a whole
+// iteration (K1 sample + exact cross-block sum into the exchange words ->
+// [all-reduce] -> K3b round -> K4 adapt/combine).  Everything here is
+// stream-ordered; a whole
 // integrate() run is enqueued without a host synchronisation (the device
 // `stop` flag turns iterations after convergence into no-ops).
 #pragma once
@@ -158,8 +159,6 @@ class Context {
   std::uint64_t launches = 0;
 
   DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var, scalars, point;
-  DevBuf<std::uint32_t> partials;            ///< K1 bin partials [block][word][slot]
-  DevBuf<unsigned long long> scal_partials;  ///< K1 est+/est-/var partials [block][kind][word]
   DevBuf<unsigned long long> words, err_key;
   DevBuf<RunState> state;
   DevBuf<unsigned int> counter;  ///< finish-kernel last-block counter (self-resetting)
@@ -211,10 +210,10 @@ class Context {
 struct Launch {
   int blocks = 0;
   std::size_t smem = 0;
-  std::uint32_t pnb = 0;  ///< partial cells per axis (n_bins, +1 padding cell on the Philox path)
+  std::uint32_t pnb = 0;  ///< histogram cells per axis (n_bins, +1 padding cell on the Philox path)
 };
 
-/// Cells per axis in K1's shared histogram and partials for a stream kind.
+/// Cells per axis in K1's shared histogram for a stream kind.
 constexpr std::uint32_t partial_bins(RngKind r, std::uint32_t nb) { return nb + (r == RngKind::philox ? 1u : 0u); }
 
 /// The work-index -> cube map of K1 (see vsample_kernel): whole rows along
@@ -244,7 +243,7 @@ inline void set_fast_constants(SampleArgs& a, const Shape& sh, int D) {
 template <class F, int D, RngKind R, int NB = 0>
 Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes,
                  std::uint64_t iter_root, std::uint64_t n0, std::uint64_t n1, const int* stop,
-                 unsigned long long* err_key) {
+                 unsigned long long* err_key, unsigned long long* words) {
   auto kern = vsample_kernel<F, D, R, NB>;
   constexpr int kThreads = sample_threads(R, D);
   constexpr int kWalkers = kThreads;  // threads that walk cubes
@@ -320,8 +319,9 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
       if (j < static_cast<int>(sh.dims)) st /= sh.g;
     }
   }
-  a.partials = ctx.partials.ensure(static_cast<std::size_t>(L.blocks) * kXWords * (bin_axes * L.pnb) + 1);
-  a.scal_partials = ctx.scal_partials.ensure(static_cast<std::size_t>(L.blocks) * kScalarAccs * kXWords);
+  if (!words) throw std::invalid_argument("K1: the exchange buffer must be provided");
+  a.words = words;
+  a.nb_out = sh.nb;
   a.err_key = err_key;
   a.stop = stop;
   kern<<<L.blocks, kThreads, L.smem, ctx.stream()>>>(a, f);
@@ -363,13 +363,15 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
 
 template <class F, RngKind R>
 Launch dispatch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_axes, std::uint64_t iter_root,
-                   std::uint64_t n0, std::uint64_t n1, const int* stop, unsigned long long* err_key) {
+                   std::uint64_t n0, std::uint64_t n1, const int* stop, unsigned long long* err_key,
+                   unsigned long long* words) {
   switch (sh.dims) {
 #define MCB_CASE(D) \
   case D:           \
     if constexpr (D <= MCB_DIMS_MAX) {                                                                                  \
-      if (sh.nb == 50) return launch_k1<F, D, R, 50>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key);          \
-      return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key);                            \
+      if (sh.nb == 50)                                                                                                \
+        return launch_k1<F, D, R, 50>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);               \
+      return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);                  \
     }                                                                                                                   \
     break;
     MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
@@ -396,24 +398,6 @@ void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t ite
       break;
   }
   throw std::invalid_argument("B200 path: no kernel compiled for dims=" + std::to_string(sh.dims));
-}
-
-/// K3a: per-block partials -> exchange words (zeroed first; chunks of blocks
-/// meet in exact 64-bit integer atomics).
-inline void launch_reduce(Context& ctx, const Launch& L, std::uint32_t bin_axes, std::uint32_t nb,
-                          unsigned long long* words, const int* stop, bool words_zeroed = false) {
-  const int nbins = static_cast<int>(bin_axes * nb);
-  const int n = (nbins + kScalarAccs) * kXWords;
-  if (!words_zeroed) MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * n, ctx.stream()));
-  const std::uint32_t pnb = L.pnb ? L.pnb : nb;
-  const int npart = (static_cast<int>(bin_axes * pnb) + kScalarAccs) * kXWords;
-  const int chunks = std::max(1, std::min(L.blocks, 16));
-  const dim3 grid((npart + 255) / 256, chunks);
-  reduce_partials_kernel<0><<<grid, 256, 0, ctx.stream()>>>(ctx.partials.get(), ctx.scal_partials.get(), L.blocks,
-                                                             static_cast<int>(bin_axes * pnb), static_cast<int>(pnb),
-                                                             static_cast<int>(nb), words, stop);
-  MCB_CUDA(cudaGetLastError());
-  ++ctx.launches;
 }
 
 /// Warps of a finish/adjust block that adapt axes (one axis each); their

@@ -1,13 +1,11 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// K3a (cross-block exact reduction) and the fused "finish" kernel K3b+K4
-// (exact rounding, on-device grid adaptation, inverse-variance combination,
-// chi^2 and the convergence gate).  Together with K1 they make one m-Cubes
-// iteration with no host round trip.
-//
-// K3a sums the per-block partials into the exchange buffer (unnormalised u64
-// digit sums -- integer, so exact and order-free; under multi-GPU this buffer
-// is what NCCL all-reduces).  The finish kernel rounds each accumulator to
+// The fused "finish" kernel K3b+K4 (exact rounding, on-device grid
+// adaptation, inverse-variance combination, chi^2 and the convergence gate).
+// Together with K1 -- whose blocks add their exact accumulators into the
+// exchange buffer (unnormalised u64 digit sums: integer, so exact and
+// order-free; under multi-GPU this buffer is what NCCL all-reduces) -- it makes
+// one m-Cubes iteration with no host round trip.  The finish kernel rounds each accumulator to
 // the nearest double exactly like ExactSum::value() (exact_sum.hpp:137-179),
 // producing v_sample's outputs (sampler.hpp:322-332), then replaces
 // Grid::adjusted / adjusted_symmetric (grid.hpp:104-146, 232-297),
@@ -37,46 +35,6 @@ struct RunState {
 /// Exchange-buffer slots: est+, est-, var, then bin_axes*nb bins.
 MCB_HD int exchange_accs(std::uint32_t bin_axes, std::uint32_t nb) {
   return kScalarAccs + static_cast<int>(bin_axes * nb);
-}
-
-// ------------------------------------------------------------------ K3a
-/// Per-block partial layouts written by K1:
-///   bins    [block][word][slot]  u32 digits (slot = axis*nb + bin), coalesced over slots
-///   scalars [block][kind][word]  u64 sums of the 32 lane copies (kind = est+, est-, var)
-/// K3a sums them over blocks into the exchange buffer (zeroed beforehand).
-/// Blocks are split into `gridDim.y` chunks whose sums meet in 64-bit integer
-/// atomics: integer addition, so exact and order-free.
-/// Partial slots c = axis*pnb + cell; cells >= nb (the Philox path's padding
-/// cell) fold into bin nb-1 of the exchange buffer.
-template <int kTag = 0>
-__global__ void reduce_partials_kernel(const std::uint32_t* __restrict__ bins, const unsigned long long* __restrict__ scal,
-                                       int nblocks, int nbins, int pnb, int nb, unsigned long long* __restrict__ words,
-                                       const int* stop) {
-  if (stop && *stop) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nbin_words = nbins * kXWords, nscal_words = kScalarAccs * kXWords;
-  if (idx >= nbin_words + nscal_words) return;
-  const int chunk = (nblocks + gridDim.y - 1) / gridDim.y;
-  const int b0 = blockIdx.y * chunk, b1 = min(nblocks, b0 + chunk);
-  unsigned long long s0 = 0, s1 = 0;
-  if (idx < nbin_words) {  // idx = w * nbins + c
-    const std::size_t stride = static_cast<std::size_t>(nbin_words);
-    int b = b0;
-    for (; b + 2 <= b1; b += 2) {
-      s0 += bins[(b + 0) * stride + idx];
-      s1 += bins[(b + 1) * stride + idx];
-    }
-    if (b < b1) s0 += bins[b * stride + idx];
-    const unsigned long long s = s0 + s1;
-    const int w = idx / nbins, c = idx % nbins;
-    const int ax = c / pnb, cell = c % pnb;
-    const int slot = ax * nb + (cell < nb ? cell : nb - 1);
-    if (s) atomicAdd(words + (kScalarAccs + slot) * kXWords + w, s);
-  } else {  // idx - nbin_words = kind * kXWords + w
-    const int j = idx - nbin_words;
-    for (int b = b0; b < b1; ++b) s0 += scal[static_cast<std::size_t>(b) * nscal_words + j];
-    if (s0) atomicAdd(words + j, s0);
-  }
 }
 
 // ------------------------------------------------------------------ grid adaptation
@@ -362,7 +320,7 @@ struct RoundArgs {
   double* var;       ///< 1 double
   double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
   const int* stop;
-  int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K3a (integrate loop)
+  int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K1 flush (integrate loop)
 };
 
 struct EpilogueArgs {
@@ -445,7 +403,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
     return;
   }
   if (threadIdx.x == 0) MCB_FIN_STAMP(3);
-  // every block has read its words: ready the buffer for the next K3a, on the
+  // every block has read its words: ready the buffer for the next K1 flush, on the
   // warps the adaptation leaves idle (all threads afterwards if none is idle)
   const int nzero = (kScalarAccs + nbins) * kXWords;
   const int busy = 32 * (e.adjusting ? e.adj_warps : 1);

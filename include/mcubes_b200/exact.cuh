@@ -14,7 +14,7 @@
 // geometry, any cube partition across GPUs, and equal to the reference's
 // ExactSum::value() after rounding.
 //
-// Exchange format (per-block partials, the NCCL all-reduce buffer and the
+// Exchange format (K1's flush target, the NCCL all-reduce buffer and the
 // oracle's mcubes_oracle.c): kXWords unsigned 64-bit words per accumulator,
 // each an unnormalised sum of radix-2^32 digits.  Integer sums of that form are
 // associative, so the cross-GPU all-reduce is exact too.

@@ -133,7 +133,7 @@ inline Context& default_context() {
 /// orchestration below serve every functor type.
 struct IntegrandOps {
   std::function<Launch(Context&, const Shape&, std::uint32_t, std::uint64_t, std::uint64_t, std::uint64_t,
-                       const int*, unsigned long long*)>
+                       const int*, unsigned long long*, unsigned long long*)>  // ..., stop, err_key, exchange words
       k1;
   std::function<void(Context&, const Shape&, std::uint64_t, std::uint64_t, std::uint64_t, double*, double*)> point;
   RngKind rng = RngKind::compat;
@@ -143,8 +143,8 @@ template <DeviceIntegrand F, RngKind R = RngKind::compat>
 IntegrandOps make_ops(const F& f) {
   IntegrandOps ops;
   ops.k1 = [f](Context& c, const Shape& sh, std::uint32_t ba, std::uint64_t root, std::uint64_t n0,
-               std::uint64_t n1, const int* stop, unsigned long long* err) {
-    return dispatch_k1<F, R>(c, f, sh, ba, root, n0, n1, stop, err);
+               std::uint64_t n1, const int* stop, unsigned long long* err, unsigned long long* words) {
+    return dispatch_k1<F, R>(c, f, sh, ba, root, n0, n1, stop, err, words);
   };
   ops.point = [f](Context& c, const Shape& sh, std::uint64_t root, std::uint64_t t, std::uint64_t k, double* x,
                   double* fx) { dispatch_point<F, R>(c, f, sh, root, t, k, x, fx); };
@@ -390,9 +390,10 @@ inline SampleResult sample_once(Context& ctx, const IntegrandOps& ops, const Gri
   unsigned long long* err = ctx.err_key.ensure(1);
   MCB_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream()));
   const std::uint64_t root = iteration_key(seed, iteration);
-  const Launch L = ops.k1(ctx, sh, bin_axes, root, 0, m, nullptr, err);
-  unsigned long long* words = ctx.words.ensure(static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords);
-  launch_reduce(ctx, L, bin_axes, sh.nb, words, nullptr);
+  const std::size_t nwords = static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords;
+  unsigned long long* words = ctx.words.ensure(nwords);
+  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * nwords, ctx.stream()));
+  (void)ops.k1(ctx, sh, bin_axes, root, 0, m, nullptr, err, words);  // K1 flushes straight into the words
   double* sc = ctx.scalars.ensure(2);
   double* contrib = bin_axes ? ctx.contrib.ensure(n) : nullptr;
   launch_finish(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr, nullptr);
@@ -695,18 +696,25 @@ class Run {
   const int* stop_flag() const { return &ctx_.state.get()->stop; }
 
   /// K1 over the work slice [n0, n1) of the linear work index (default: all cubes).
+  /// K1 over the work slice [n0, n1) of the linear work index (default: all
+  /// cubes).  Its blocks flush straight into exchange(): after sample() the
+  /// exchange words hold this slice's sums (the words are zeroed first unless
+  /// finish() already left them zero).
   void sample(std::uint32_t it, std::uint64_t n0 = 0, std::uint64_t n1 = ~0ull) {
     if (n1 > sh_.m) n1 = sh_.m;
-    last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get());
+    if (!words_clean_) zero_exchange();
+    last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get(),
+                    words_);
+    words_clean_ = false;
     last_it_ = it;
   }
 
-  /// K3a: this device's per-block partials -> exchange words.
+  /// The cross-block reduction (the reference's in-process exact merge,
+  /// sampler.hpp:272-276).  K1's blocks already added their words into the
+  /// exchange buffer, so this only checks the call order; the entry point
+  /// stays for the stepped API (mcb_run_reduce).
   void reduce(std::uint32_t it) {
     if (it != last_it_) throw std::invalid_argument("reduce: iteration was not sampled");
-    // overwrite semantics; the memset is skipped when finish() left the words zeroed
-    launch_reduce(ctx_, last_, bin_axes(it), sh_.nb, words_, stop_flag(), words_clean_);
-    words_clean_ = false;
   }
 
   /// K3b + K4 (one fused kernel) for iteration it, after the optional

@@ -24,8 +24,8 @@
 //    EXACTLY into shared-memory superaccumulators (exact.cuh): no global atomics,
 //    results independent of launch geometry and of how cubes are split across
 //    GPUs, and equal to the reference's ExactSum reductions.
-//  * At the end each block writes its accumulators (plain coalesced stores) as
-//    a per-block partial; K3 (epilogue.cuh) sums the partials.
+//  * At the end each block adds its nonzero accumulator words into the
+//    exchange buffer (exact 64-bit integer atomics; see the flush below).
 #pragma once
 
 #include <cmath>
@@ -69,8 +69,8 @@ struct SampleArgs {
   std::uint64_t R;                      ///< rows m / g
   std::uint64_t stepR;                  ///< row mode: (T*A) mod R, A = A' = 1 + g + ... + g^(D-2)
   std::uint32_t round_keys[20];         ///< philox: (k0, k1) of rounds 0..9 (uniform; folded into LOP3)
-  std::uint32_t* partials;             ///< bins: [gridDim][kXWords][bin_axes*nb] u32
-  unsigned long long* scal_partials;   ///< est+/est-/var: [gridDim][3][kXWords] u64 (lane copies folded)
+  unsigned long long* words;  ///< exchange buffer (zeroed): every block adds its nonzero words here
+  std::uint32_t nb_out;       ///< n_bins of the exchange layout (the padding cell folds into bin nb_out-1)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
 };
@@ -117,7 +117,7 @@ __device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
 /// to one rounding).
 /// The table has nb + 1 entries per axis: entry nb repeats bin nb-1, so a
 /// bin coordinate that rounds up to exactly nb (possible only for g >= 2^20)
-/// needs no clamp -- its deposit lands in a padding cell that K3a folds into
+/// needs no clamp -- its deposit lands in a padding cell that K1's flush folds into
 /// bin nb-1 (philox_pnb).
 template <int D>
 __device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a) {
@@ -475,22 +475,32 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   }
   __syncthreads();
 
-  // per-block partials.  Bins: [block][word][slot] u32, coalesced over slots.
-  // Scalars: the 32 lane copies folded into u64 word sums (< 2^37, exact).
-  const int nbins = static_cast<int>(a.bin_axes * nb);
-  std::uint32_t* out = a.partials + static_cast<std::size_t>(blockIdx.x) * kXWords * nbins;
-  for (int i = tid; i < nbins * kXWords; i += nt) {
-    const int w = i / nbins, c = i % nbins;
-    out[i] = bins[c * kXWords + w];
-  }
-  unsigned long long* sout = a.scal_partials + static_cast<std::size_t>(blockIdx.x) * kScalarAccs * kXWords;
-  for (int i = tid; i < kScalarAccs * kXWords; i += nt) {
-    const int kind = i / kXWords, w = i % kXWords;
-    const std::uint32_t* src = acc + kind * kLaneCopies * kXWords + w;
-    unsigned long long s = 0;
+  // Flush: the block's nonzero words go straight into the exchange buffer as
+  // exact 64-bit integer adds -- a few thousand per block per iteration,
+  // against the ~10^8 shared-memory deposits they summarise -- so no
+  // per-block partials are written and no separate reduction pass reads them
+  // back.  Integer addition is order-free: bit-reproducible for any launch
+  // geometry and GPU count.  (The reference merges per-worker ExactSums in
+  // worker order, sampler.hpp:272-276; the integer sum is the same.)
+  {
+    const int ncells = static_cast<int>(a.bin_axes * nb);
+    for (int i = tid; i < ncells * kXWords; i += nt) {
+      const std::uint32_t v = bins[i];
+      if (!v) continue;
+      const int c = i / kXWords, w = i - c * kXWords;
+      const int ax = c / static_cast<int>(nb), cell = c - ax * static_cast<int>(nb);
+      const int slot = ax * static_cast<int>(a.nb_out) + min(cell, static_cast<int>(a.nb_out) - 1);
+      atomicAdd(a.words + static_cast<std::size_t>(kScalarAccs + slot) * kXWords + w, static_cast<unsigned long long>(v));
+    }
+    // est+/est-/var: the 32 lane copies folded into u64 word sums (< 2^37, exact)
+    for (int i = tid; i < kScalarAccs * kXWords; i += nt) {
+      const int kind = i / kXWords, w = i % kXWords;
+      const std::uint32_t* src = acc + kind * kLaneCopies * kXWords + w;
+      unsigned long long sum = 0;
 #pragma unroll 8
-    for (int l = 0; l < kLaneCopies; ++l) s += src[l * kXWords];
-    sout[i] = s;
+      for (int l = 0; l < kLaneCopies; ++l) sum += src[l * kXWords];
+      if (sum) atomicAdd(a.words + i, sum);
+    }
   }
 }
 
