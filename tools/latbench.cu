@@ -1,14 +1,45 @@
 // Per-phase device time of one small-ncall iteration (BASELINE C1: 5D f4,
 // 1e6 calls) through gpu::Run, CUDA events between the phases.
 //   ./latbench [rng 0|1] [maxcalls] [dims]
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "mcubes_b200/mcubes.cuh"
 
 using namespace mcubes;
 
+static int fixed_cost() {
+  gpu::Context ctx(0);
+  const gpu::fn::F4 f{};
+  const gpu::IntegrandOps ops = gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox>(f);
+  for (std::uint32_t its : {1u, 2u, 20u}) {
+    RunConfig cfg;
+    cfg.dims = 5;
+    cfg.maxcalls = 1000000;
+    cfg.lower.assign(5, 0.0);
+    cfg.upper.assign(5, 1.0);
+    cfg.itmax = its;
+    cfg.ita = its;
+    cfg.tau_rel = 1e-15;
+    cfg.rng = gpu::RngKind::philox;
+    (void)gpu::integrate_ops(ctx, ops, cfg);
+    double best = 1e30;
+    for (int r = 0; r < 7; ++r) {
+      ctx.sync();
+      const auto t0 = std::chrono::steady_clock::now();
+      (void)gpu::integrate_ops(ctx, ops, cfg);
+      best = std::min(best, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::printf("C++ integrate_ops itmax=%u: %.1f us\n", its, best * 1e6);
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "fixed") return fixed_cost();
   const int rngk = argc > 1 ? std::atoi(argv[1]) : 1;
   const std::uint64_t maxcalls = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1000000ull;
   const int D = argc > 3 ? std::atoi(argv[3]) : 5;
