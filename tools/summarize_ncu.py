@@ -36,8 +36,9 @@ KEYS = [
     ("smsp__inst_executed_op_shared_atom.sum", "shared atomics (warp-level)"),
     ("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", "GLOBAL atomics"),
     ("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", "GLOBAL reductions"),
-    ("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "GLOBAL atomic requests (histogram path must be 0)"),
-    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "GLOBAL reduction requests (must be 0)"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "GLOBAL atomic requests (none on the histogram path)"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+     "GLOBAL reduction requests (only the per-block flush of nonzero exchange words; per-sample deposits stay in shared memory)"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smem atomic bank conflicts"),
     ("dram__bytes_read.sum", "DRAM bytes read"),
     ("dram__bytes_write.sum", "DRAM bytes written"),
