@@ -214,9 +214,12 @@ int mcb_run_resume(mcb_run* run, const double* edges, const mcb_iteration* done,
 void* mcb_run_exchange_ptr(const mcb_run* run);
 /* Total linear work items (= m cubes). */
 uint64_t mcb_run_work_items(const mcb_run* run);
-/* K1: sample work items [n0, n1) of iteration it. */
+/* K1: sample work items [n0, n1) of iteration it; its blocks add their exact
+ * sums into the exchange buffer (which then holds exactly this slice's sums). */
 int mcb_run_sample(mcb_run* run, uint32_t it, uint64_t n0, uint64_t n1);
-/* K3a: exact cross-block sum into the exchange buffer (all-reduce it next). */
+/* The cross-block reduction step of the reference's merge (sampler.hpp:272-276):
+ * already done by K1's flush; kept so stepped callers read sample -> reduce ->
+ * all-reduce -> finish.  Checks that `it` was sampled. */
 int mcb_run_reduce(mcb_run* run, uint32_t it);
 /* K3b + K4: round, adapt the grid, combine, convergence gate. */
 int mcb_run_finish(mcb_run* run, uint32_t it);
