@@ -430,4 +430,44 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   }
 }
 
+// ------------------------------------------------------------------ run setup / collect
+/// One launch instead of three uploads and three memsets per integrate():
+/// grid edges and bounds come straight from pinned host memory (zero-copy),
+/// the run state and the exchange words are zeroed, the error key set.
+template <int kTag = 0>
+__global__ void run_init_kernel(const double* __restrict__ staged, std::uint32_t n_edges, std::uint32_t dims,
+                                double* edges, double* lower, double* upper, RunState* st, unsigned long long* err_key,
+                                unsigned long long* words, std::uint32_t n_words) {
+  const std::uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (std::uint32_t i = i0; i < n_edges; i += stride) edges[i] = staged[i];
+  for (std::uint32_t i = i0; i < dims; i += stride) {
+    lower[i] = staged[n_edges + i];
+    upper[i] = staged[n_edges + dims + i];
+  }
+  for (std::uint32_t i = i0; i < n_words; i += stride) words[i] = 0ull;
+  if (i0 == 0) {
+    *st = RunState{};
+    *err_key = ~0ull;
+  }
+}
+
+/// One launch instead of four device-to-host copies at the end of a run: the
+/// run state, the first non-finite key and the history land in pinned host
+/// memory (zero-copy writes), read after one stream synchronisation.
+template <int kTag = 0>
+__global__ void run_collect_kernel(const RunState* st, const unsigned long long* err_key, const double* hist_est,
+                                   const double* hist_var, std::uint32_t itmax, unsigned char* out) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  auto* hs = reinterpret_cast<double*>(out + sizeof(RunState) + 8);
+  const std::uint32_t n = st->iterations_used < itmax ? st->iterations_used : itmax;
+  if (i < n) {
+    hs[i] = hist_est[i];
+    hs[itmax + i] = hist_var[i];
+  }
+  if (i == 0) {
+    *reinterpret_cast<RunState*>(out) = *st;
+    *reinterpret_cast<unsigned long long*>(out + sizeof(RunState)) = *err_key;
+  }
+}
+
 }  // namespace mcubes::gpu

@@ -599,32 +599,36 @@ class Run {
     ctx_.activate();
     const Grid g0(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper);
     const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
+    ctx_.contrib.ensure(n);
+    ctx_.hist_est.ensure(cfg_.itmax);
+    ctx_.hist_var.ensure(cfg_.itmax);
+    ctx_.state.ensure(1);
+    ctx_.err_key.ensure(1);
+    words_ = ctx_.words.ensure(exchange_words(cfg_.dims));
     if (sizeof(double) * (n + 2 * cfg_.dims) <= Context::kPinnedBytes) {
-      // asynchronous copies from the pinned staging buffer (pageable sources
-      // would block the host for each)
-      ctx_.staging_wait();  // an earlier Run's copies may still read the buffer
+      // one launch: the kernel reads the staged grid from pinned host memory
+      // and zeroes the state and the exchange words
+      ctx_.staging_wait();  // an earlier Run's setup may still read the buffer
       auto* pin = reinterpret_cast<double*>(ctx_.pinned());
       std::memcpy(pin, g0.raw_edges().data(), sizeof(double) * n);
       std::memcpy(pin + n, cfg_.lower.data(), sizeof(double) * cfg_.dims);
       std::memcpy(pin + n + cfg_.dims, cfg_.upper.data(), sizeof(double) * cfg_.dims);
-      MCB_CUDA(cudaMemcpyAsync(ctx_.edges.ensure(n), pin, sizeof(double) * n, cudaMemcpyHostToDevice, ctx_.stream()));
-      MCB_CUDA(cudaMemcpyAsync(ctx_.lower.ensure(cfg_.dims), pin + n, sizeof(double) * cfg_.dims,
-                               cudaMemcpyHostToDevice, ctx_.stream()));
-      MCB_CUDA(cudaMemcpyAsync(ctx_.upper.ensure(cfg_.dims), pin + n + cfg_.dims, sizeof(double) * cfg_.dims,
-                               cudaMemcpyHostToDevice, ctx_.stream()));
+      const auto nw = static_cast<std::uint32_t>(exchange_words(cfg_.dims));
+      run_init_kernel<0><<<std::max<std::uint32_t>(1, (nw + 255) / 256), 256, 0, ctx_.stream()>>>(
+          pin, static_cast<std::uint32_t>(n), cfg_.dims, ctx_.edges.ensure(n), ctx_.lower.ensure(cfg_.dims),
+          ctx_.upper.ensure(cfg_.dims), ctx_.state.get(), ctx_.err_key.get(), words_, nw);
+      MCB_CUDA(cudaGetLastError());
+      ++ctx_.launches;
       ctx_.staging_recorded();
+      words_clean_ = true;
     } else {
       upload(ctx_, ctx_.edges, g0.raw_edges().data(), n);
       upload(ctx_, ctx_.lower, cfg_.lower.data(), cfg_.dims);
       upload(ctx_, ctx_.upper, cfg_.upper.data(), cfg_.dims);
+      MCB_CUDA(cudaMemsetAsync(ctx_.state.get(), 0, sizeof(RunState), ctx_.stream()));
+      MCB_CUDA(cudaMemsetAsync(ctx_.err_key.get(), 0xff, sizeof(unsigned long long), ctx_.stream()));
+      zero_exchange();
     }
-    ctx_.contrib.ensure(n);
-    ctx_.hist_est.ensure(cfg_.itmax);
-    ctx_.hist_var.ensure(cfg_.itmax);
-    MCB_CUDA(cudaMemsetAsync(ctx_.state.ensure(1), 0, sizeof(RunState), ctx_.stream()));
-    MCB_CUDA(cudaMemsetAsync(ctx_.err_key.ensure(1), 0xff, sizeof(unsigned long long), ctx_.stream()));
-    words_ = ctx_.words.ensure(exchange_words(cfg_.dims));
-    zero_exchange();
   }
 
   /// Resume from a checkpoint: the grid in force after `history.size()`
@@ -772,12 +776,11 @@ class Run {
     unsigned long long key = ~0ull;
     std::vector<double> e, v;
     if (staged) {
-      MCB_CUDA(cudaMemcpyAsync(pin, ctx_.state.get(), sizeof(RunState), cudaMemcpyDeviceToHost, ctx_.stream()));
-      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState), ctx_.err_key.get(), 8, cudaMemcpyDeviceToHost, ctx_.stream()));
-      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState) + 8, ctx_.hist_est.get(), hbytes, cudaMemcpyDeviceToHost,
-                               ctx_.stream()));
-      MCB_CUDA(cudaMemcpyAsync(pin + sizeof(RunState) + 8 + hbytes, ctx_.hist_var.get(), hbytes,
-                               cudaMemcpyDeviceToHost, ctx_.stream()));
+      ctx_.staging_wait();
+      run_collect_kernel<0><<<std::max<std::uint32_t>(1, (cfg_.itmax + 255) / 256), 256, 0, ctx_.stream()>>>(
+          ctx_.state.get(), ctx_.err_key.get(), ctx_.hist_est.get(), ctx_.hist_var.get(), cfg_.itmax, pin);
+      MCB_CUDA(cudaGetLastError());
+      ++ctx_.launches;
       ctx_.sync();
       std::memcpy(&st, pin, sizeof st);
       std::memcpy(&key, pin + sizeof(RunState), 8);
