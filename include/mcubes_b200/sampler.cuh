@@ -3,27 +3,28 @@
 // K1: the m-Cubes sampling kernel (V-Sample / V-Sample-No-Adjust).
 //
 // Replaces run_cube + sample_all_cubes (sampler.hpp:147-181, 213-278) and the
-// paper's atomics-based CUDA V-Sample.  Design:
+// paper's atomics-based CUDA V-Sample.  Design (DESIGN.md
+// section 4):
 //
-//  * Persistent grid, one 512-thread block per SM.  Work is a range [n0, n1) of
-//    a linear index n; cube t = n*A mod m with A = 1 + g + ... + g^(d-1)
-//    (a bijection because A = 1 mod g).  Neighbouring lanes therefore sit in
-//    cubes whose digits differ by one on EVERY axis, which spreads their bin
-//    deposits over distinct shared-memory words.  Digits advance per thread by
-//    an odometer add of the constant step (T*A mod m), so the per-cube 64-bit
-//    div/mod chain of sampler.hpp:152-158 runs once per thread, not per cube.
-//  * The grid (right edges with the left boundary prepended) lives in shared
-//    memory.
-//  * Per sample, the compat path reproduces the reference arithmetic exactly:
-//    SplitMix keyed stream, (digit + r) / g, the bin map and jacobian of
-//    grid.hpp:204-224, Welford (sampler.hpp:93-104).  IEEE divisions by the
-//    launch constants g, n and p(p-1) use Markstein's correction with a
-//    correctly rounded reciprocal (q0 = a*y; r = fma(-q0, b, a); q = fma(r, y, q0)),
-//    which returns the correctly rounded quotient -- the same bits as a/b.
-//  * Estimates, variances and the d x n_bins contributions (f*J)^2 are summed
-//    EXACTLY into shared-memory superaccumulators (exact.cuh): no global atomics,
-//    results independent of launch geometry and of how cubes are split across
-//    GPUs, and equal to the reference's ExactSum reductions.
+//  * Persistent grid: one block per SM (1024 threads on the Philox path, 768
+//    on compat).  Each thread walks its share of the linear work index n in
+//    whole rows along axis 0 (row mode) or cube by cube (CubeWalk below); the
+//    n -> cube map is a bijection that spreads neighbouring lanes over distinct
+//    bins on every axis and depends on (m, g, d) only.
+//  * The grid lives in shared memory as per-bin {left, width} (compat) or
+//    {left - i*width, width} (Philox: the point is one FMA) pairs.
+//  * compat reproduces the reference arithmetic exactly: SplitMix keyed
+//    stream, (digit + r) / g, the bin map and jacobian of grid.hpp:204-224,
+//    Welford (sampler.hpp:93-104); IEEE divisions by the launch constants use
+//    Markstein's correction with a correctly rounded reciprocal
+//    (q0 = a*y; r = fma(-q0, b, a); q = fma(r, y, q0)), i.e. the same bits as a/b.
+//    Philox: Philox4x32-10 keyed by the iteration, 32-bit uniforms, FMA
+//    transform, restated bit for bit by oracle/mcubes_oracle.c run_cube_philox.
+//  * Estimates and variances are summed EXACTLY into shared-memory
+//    superaccumulators (exact.cuh), the d x n_bins contributions (f*J)^2 too
+//    (compat: exact values; Philox: rounded to 24 significant bits first).  No
+//    global atomics per sample; results independent of launch geometry and of
+//    how cubes are split across GPUs, and equal to the reference's ExactSum.
 //  * At the end each block adds its nonzero accumulator words into the
 //    exchange buffer (exact 64-bit integer atomics; see the flush below).
 #pragma once
