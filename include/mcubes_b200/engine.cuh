@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -38,6 +39,35 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
                     ":" + std::to_string(line));
 }
 #define MCB_CUDA(x) ::mcubes::gpu::cuda_check((x), #x, __FILE__, __LINE__)
+
+/// Programmatic dependent launch for the run's kernels (config.cuh
+/// pdl_wait/pdl_trigger); MCB_PDL=0 in the environment turns it off.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MCB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+/// kern<<<grid, block, smem, stream>>>(args...) with programmatic stream
+/// serialisation (the kernel must pdl_wait() before reading its
+/// predecessor's output).
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
+                Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  MCB_CUDA(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
+}
 
 template <class T>
 class DevBuf {
@@ -324,8 +354,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.nb_out = sh.nb;
   a.err_key = err_key;
   a.stop = stop;
-  kern<<<L.blocks, kThreads, L.smem, ctx.stream()>>>(a, f);
-  MCB_CUDA(cudaGetLastError());
+  launch_pdl(kern, L.blocks, kThreads, L.smem, ctx.stream(), a, f);
   ++ctx.launches;
   return L;
 }
@@ -449,9 +478,8 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   }
   const int values = static_cast<int>(sh.dims * sh.nb + 2);  // one warp per output value
   const int warps_per_block = kFinishThreads / 32;
-  finish_kernel<0><<<(values + warps_per_block - 1) / warps_per_block, kFinishThreads, smem, ctx.stream()>>>(
-      r, e, epi ? 1 : 0, counter);
-  MCB_CUDA(cudaGetLastError());
+  launch_pdl(finish_kernel<0>, (values + warps_per_block - 1) / warps_per_block, kFinishThreads, smem, ctx.stream(), r,
+             e, epi ? 1 : 0, counter);
   ++ctx.launches;
 }
 

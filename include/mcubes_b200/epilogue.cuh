@@ -351,6 +351,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
                                                                 int with_epilogue, unsigned int* counter) {
   extern __shared__ double fin_smem[];
   __shared__ bool is_last;
+  pdl_trigger();  // the next iteration's K1 may launch (it waits for this grid)
+  pdl_wait();     // K1's flushed words (or the all-reduce's) are complete
   if (blockIdx.x == 0 && threadIdx.x == 0) MCB_FIN_STAMP(0);
   const int stop0 = r.stop ? *r.stop : 0;
   __syncthreads();  // every thread reads `stop` before the last block may set it
@@ -438,6 +440,8 @@ template <int kTag = 0>
 __global__ void run_init_kernel(const double* __restrict__ staged, std::uint32_t n_edges, std::uint32_t dims,
                                 double* edges, double* lower, double* upper, RunState* st, unsigned long long* err_key,
                                 unsigned long long* words, std::uint32_t n_words) {
+  pdl_trigger();
+  pdl_wait();  // an earlier run on this context may still read the buffers written here
   const std::uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   for (std::uint32_t i = i0; i < n_edges; i += stride) edges[i] = staged[i];
   for (std::uint32_t i = i0; i < dims; i += stride) {
@@ -457,6 +461,8 @@ __global__ void run_init_kernel(const double* __restrict__ staged, std::uint32_t
 template <int kTag = 0>
 __global__ void run_collect_kernel(const RunState* st, const unsigned long long* err_key, const double* hist_est,
                                    const double* hist_var, std::uint32_t itmax, unsigned char* out) {
+  pdl_trigger();
+  pdl_wait();
   const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   auto* hs = reinterpret_cast<double*>(out + sizeof(RunState) + 8);
   const std::uint32_t n = st->iterations_used < itmax ? st->iterations_used : itmax;

@@ -614,10 +614,10 @@ class Run {
       std::memcpy(pin + n, cfg_.lower.data(), sizeof(double) * cfg_.dims);
       std::memcpy(pin + n + cfg_.dims, cfg_.upper.data(), sizeof(double) * cfg_.dims);
       const auto nw = static_cast<std::uint32_t>(exchange_words(cfg_.dims));
-      run_init_kernel<0><<<std::max<std::uint32_t>(1, (nw + 255) / 256), 256, 0, ctx_.stream()>>>(
-          pin, static_cast<std::uint32_t>(n), cfg_.dims, ctx_.edges.ensure(n), ctx_.lower.ensure(cfg_.dims),
-          ctx_.upper.ensure(cfg_.dims), ctx_.state.get(), ctx_.err_key.get(), words_, nw);
-      MCB_CUDA(cudaGetLastError());
+      launch_pdl(run_init_kernel<0>, std::max<std::uint32_t>(1, (nw + 255) / 256), 256, 0, ctx_.stream(),
+                 static_cast<const double*>(pin), static_cast<std::uint32_t>(n), cfg_.dims, ctx_.edges.ensure(n),
+                 ctx_.lower.ensure(cfg_.dims), ctx_.upper.ensure(cfg_.dims), ctx_.state.get(), ctx_.err_key.get(),
+                 words_, nw);
       ++ctx_.launches;
       ctx_.staging_recorded();
       words_clean_ = true;
@@ -777,9 +777,10 @@ class Run {
     std::vector<double> e, v;
     if (staged) {
       ctx_.staging_wait();
-      run_collect_kernel<0><<<std::max<std::uint32_t>(1, (cfg_.itmax + 255) / 256), 256, 0, ctx_.stream()>>>(
-          ctx_.state.get(), ctx_.err_key.get(), ctx_.hist_est.get(), ctx_.hist_var.get(), cfg_.itmax, pin);
-      MCB_CUDA(cudaGetLastError());
+      launch_pdl(run_collect_kernel<0>, std::max<std::uint32_t>(1, (cfg_.itmax + 255) / 256), 256, 0, ctx_.stream(),
+                 static_cast<const RunState*>(ctx_.state.get()), static_cast<const unsigned long long*>(ctx_.err_key.get()),
+                 static_cast<const double*>(ctx_.hist_est.get()), static_cast<const double*>(ctx_.hist_var.get()),
+                 cfg_.itmax, pin);
       ++ctx_.launches;
       ctx_.sync();
       std::memcpy(&st, pin, sizeof st);

@@ -332,7 +332,7 @@ struct CubeWalk {
 /// and every BASELINE config), 0 = runtime n_bins.
 template <class F, int D, RngKind R, int NB = 0>
 __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const SampleArgs a, const F f) {
-  if (a.stop && *a.stop) return;
+  pdl_trigger();  // the finish kernel may launch now; it waits for this grid to complete
   extern __shared__ __align__(16) unsigned char smem[];
   // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
   const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (R == RngKind::philox ? 1u : 0u);
@@ -345,9 +345,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   {  // zero the accumulators, stage the grid and the Welford reciprocals
     const int nwords = nacc * kXWords;
     for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
+    for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
+    pdl_wait();  // the grid, the stop flag and the exchange words come from the previous kernels
+    if (a.stop && *a.stop) return;  // (uniform across the block)
     if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
     else stage_grid_fast<D>(LW, a);
-    for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
   }
   __syncthreads();
 

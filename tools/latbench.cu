@@ -38,8 +38,66 @@ static int fixed_cost() {
   return 0;
 }
 
+// Upper bound on what a CUDA graph could save: the C1 loop (10 adjusting
+// iterations) enqueued on the stream vs the same launches captured once into
+// a graph and replayed (state reset inside; device time with events).
+static int graph_gain() {
+  gpu::Context ctx(0);
+  const gpu::fn::F4 f{};
+  const gpu::IntegrandOps ops = gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox>(f);
+  RunConfig cfg;
+  cfg.dims = 5;
+  cfg.maxcalls = 1000000;
+  cfg.lower.assign(5, 0.0);
+  cfg.upper.assign(5, 1.0);
+  cfg.itmax = 10;
+  cfg.ita = 10;
+  cfg.tau_rel = 1e-15;
+  cfg.rng = gpu::RngKind::philox;
+  gpu::Run run(ctx, ops, cfg);
+  cudaStream_t s = ctx.stream();
+  auto body = [&] {
+    cudaMemsetAsync(ctx.state.get(), 0, sizeof(gpu::RunState), s);
+    for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
+      run.sample(it);
+      run.finish(it);
+    }
+  };
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto timed = [&](auto&& fn) {
+    float best = 1e30f;
+    for (int r = 0; r < 20; ++r) {
+      ctx.sync();
+      cudaEventRecord(e0, s);
+      fn();
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = std::min(best, ms);
+    }
+    return best * 1e3f;
+  };
+  const float t_stream = timed(body);
+  cudaGraph_t g;
+  MCB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  body();
+  MCB_CUDA(cudaStreamEndCapture(s, &g));
+  cudaGraphExec_t ge;
+  const auto t0 = std::chrono::steady_clock::now();
+  MCB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  const double inst_us = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e6;
+  const float t_graph = timed([&] { MCB_CUDA(cudaGraphLaunch(ge, s)); });
+  std::printf("C1 loop (10 iterations, device time): stream %.1f us  graph %.1f us  (instantiate %.1f us host)\n",
+              t_stream, t_graph, inst_us);
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "fixed") return fixed_cost();
+  if (argc > 1 && std::string(argv[1]) == "graph") return graph_gain();
   const int rngk = argc > 1 ? std::atoi(argv[1]) : 1;
   const std::uint64_t maxcalls = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1000000ull;
   const int D = argc > 3 ? std::atoi(argv[3]) : 5;
