@@ -50,6 +50,16 @@ inline bool pdl_enabled() {
   return on;
 }
 
+/// Block-wide grid adaptation in the finish kernel (adjust_grid_par);
+/// MCB_ADJ_PAR=0 selects the warp-per-axis form (same bits, for A/B timing).
+inline bool adjust_par_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MCB_ADJ_PAR");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 /// kern<<<grid, block, smem, stream>>>(args...) with programmatic stream
 /// serialisation (the kernel must pdl_wait() before reading its
 /// predecessor's output).
@@ -433,7 +443,7 @@ void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t ite
 /// scratch bounds the block's shared memory.
 inline int adjust_warps(std::uint32_t dims, std::uint32_t nb, int max_smem) {
   int w = std::max(1, std::min<int>(static_cast<int>(dims), kFinishThreads / 32));
-  const std::size_t fixed = sizeof(double) * static_cast<std::size_t>(dims) * nb;
+  const std::size_t fixed = 2 * sizeof(double) * static_cast<std::size_t>(dims) * nb;  // contributions + edges
   while (w > 1 && fixed + sizeof(double) * static_cast<std::size_t>(w) * kAdjustScratch * nb >
                       static_cast<std::size_t>(max_smem))
     --w;
@@ -463,8 +473,11 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   if (epi) {
     e = *epi;
     e.adj_warps = adjust_warps(sh.dims, sh.nb, ctx.max_smem());
-    smem = sizeof(double) *
-           (static_cast<std::size_t>(sh.dims) * sh.nb + static_cast<std::size_t>(e.adj_warps) * kAdjustScratch * sh.nb);
+    const std::size_t staged = 2 * static_cast<std::size_t>(sh.dims) * sh.nb;  // contributions + edges
+    const std::size_t par = sizeof(double) * (staged + adjust_par_scratch(sh.dims, sh.nb));
+    e.adj_par = (!e.adj.symmetric && par <= static_cast<std::size_t>(ctx.max_smem()) && adjust_par_enabled()) ? 1 : 0;
+    smem = e.adj_par ? par
+                     : sizeof(double) * (staged + static_cast<std::size_t>(e.adj_warps) * kAdjustScratch * sh.nb);
   }
   thread_local std::size_t attr_smem = 0;
   if (smem > 48 * 1024 && smem > attr_smem) {

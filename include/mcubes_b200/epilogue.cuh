@@ -74,8 +74,8 @@ __device__ __forceinline__ unsigned long long fin_now() {
 
 inline constexpr int kAdjustScratch = 6;  ///< doubles per bin of per-warp scratch
 
-__device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, const double* contrib,
-                                        std::uint32_t n, double alpha, double* scratch) {
+__device__ inline void adjust_axis_warp(double* edges_g, const double* edges_in, double lo, double hi,
+                                        const double* contrib, std::uint32_t n, double alpha, double* scratch) {
   const int lane = threadIdx.x & 31;
   double* edges = scratch;
   double* smooth = scratch + n;
@@ -84,7 +84,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
   double* T = scratch + 4 * n + 1;  // n - 1 targets
   bool any_local = false;
   for (std::uint32_t i = lane; i < n; i += 32) {
-    edges[i] = edges_g[i];
+    edges[i] = edges_in[i];
     any_local |= contrib[i] != 0.0;
   }
   const bool any = __any_sync(0xffffffffu, any_local);
@@ -117,10 +117,23 @@ __device__ inline void adjust_axis_warp(double* edges_g, double lo, double hi, c
   if (lane == 0) {  // the reference's sequential accumulations, in its order
     // rtot (grid.hpp:603-613) and the walk's cum (grid.hpp:623-626) add the
     // same imp[] in the same order, so one pass yields both: P[n] == rtot.
+    // (imp is loaded eight at a time ahead of the stores into P: the compiler
+    // cannot move a load above a possibly aliasing shared store, which would
+    // put a shared-memory round trip on every step of the dependent chain)
     double cum = 0.0;
     P[0] = 0.0;
-#pragma unroll 8
-    for (std::uint32_t k = 0; k < n; ++k) {
+    std::uint32_t k = 0;
+    for (; k + 8 <= n; k += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = imp[k + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cum += v[q];
+        P[k + 1 + q] = cum;
+      }
+    }
+    for (; k < n; ++k) {
       cum += imp[k];
       P[k + 1] = cum;
     }
@@ -191,17 +204,18 @@ struct AdjustArgs {
 };
 
 /// Grid::adjusted / adjusted_symmetric: warp j adapts axis j (symmetric: warp
-/// 0 adapts axis 0, then all warps replicate it).  `contrib` may point to
+/// 0 adapts axis 0, then all warps replicate it).  `contrib` and `edges_in`
+/// (the current edges, a copy of a.edges or a.edges itself) may point to
 /// shared or global memory.  scratch: nwarps * kAdjustScratch * nb doubles.
-__device__ inline void adjust_grid_block(const AdjustArgs& a, const double* contrib, double* scratch_all,
-                                         int adj_warps) {
+__device__ inline void adjust_grid_block(const AdjustArgs& a, const double* contrib, const double* edges_in,
+                                         double* scratch_all, int adj_warps) {
   const int warp = threadIdx.x >> 5;
   double* scratch = scratch_all + static_cast<std::size_t>(warp) * kAdjustScratch * a.nb;
   const std::uint32_t axes = a.symmetric ? 1u : a.dims;
   if (warp < adj_warps)
     for (std::uint32_t j = warp; j < axes; j += adj_warps)
-      adjust_axis_warp(a.edges + static_cast<std::size_t>(j) * a.nb, a.lower[j], a.upper[j],
-                       contrib + static_cast<std::size_t>(j) * a.nb, a.nb, a.alpha, scratch);
+      adjust_axis_warp(a.edges + static_cast<std::size_t>(j) * a.nb, edges_in + static_cast<std::size_t>(j) * a.nb,
+                       a.lower[j], a.upper[j], contrib + static_cast<std::size_t>(j) * a.nb, a.nb, a.alpha, scratch);
   if (!a.symmetric) return;
   __syncthreads();
   const double* row0 = a.edges;
@@ -220,10 +234,162 @@ __device__ inline void adjust_grid_block(const AdjustArgs& a, const double* cont
   }
 }
 
+/// Named barrier over the first `nthreads` threads of the block (a multiple of 32).
+__device__ __forceinline__ void bar_sync_n(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+/// Shared-memory doubles adjust_grid_par needs beyond the staged contributions and edges.
+MCB_HD std::size_t adjust_par_scratch(std::uint32_t dims, std::uint32_t nb) {
+  return static_cast<std::size_t>(dims) * (kAdjustScratch * nb + 4);
+}
+
+/// Grid::adjusted (grid.hpp:232-297), every axis at once across the first
+/// `nthreads` threads of the block: the element-wise steps (smoothing, the
+/// importance r_i, the equal-share walk, the monotonicity check) run one
+/// element per thread, and the three order-dependent sums of each axis (the
+/// smoothed total, the cumulative importance, the targets) run one axis per
+/// lane of warp 0 -- the reference's sequential accumulations in its order,
+/// all axes in lockstep.  Bitwise the same edges as adjust_axis_warp.
+/// contrib_s and edges_s are staged in shared memory; scratch:
+/// adjust_par_scratch(dims, nb) doubles.
+__device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contrib_s, const double* edges_s,
+                                       double* scratch, int nthreads) {
+  const std::uint32_t n = a.nb, D = a.dims;
+  const int tid = threadIdx.x;
+  double* tot = scratch + static_cast<std::size_t>(D) * kAdjustScratch * n;
+  double* lo = tot + D;
+  double* hi = lo + D;
+  int* any = reinterpret_cast<int*>(hi + D);
+  int* bad = any + D;
+  auto smooth_of = [&](std::uint32_t j) { return scratch + static_cast<std::size_t>(j) * kAdjustScratch * n; };
+  if (tid < static_cast<int>(D)) {
+    lo[tid] = a.lower[tid];
+    hi[tid] = a.upper[tid];
+    any[tid] = 0;
+    bad[tid] = 0;
+  }
+  bar_sync_n(1, nthreads);
+  const std::uint32_t total_el = D * n;
+  for (std::uint32_t idx = tid; idx < total_el; idx += nthreads) {  // smoothing (grid.hpp:240-252)
+    const std::uint32_t j = idx / n, i = idx - j * n;
+    const double* c = contrib_s + static_cast<std::size_t>(j) * n;
+    if (c[i] != 0.0) any[j] = 1;
+    if (n == 1) continue;
+    double v;
+    if (i == 0) v = 0.5 * (c[0] + c[1]);
+    else if (i + 1 == n) v = 0.5 * (c[n - 2] + c[n - 1]);
+    else v = (c[i - 1] + c[i] + c[i + 1]) / 3.0;
+    smooth_of(j)[i] = v;
+  }
+  bar_sync_n(1, nthreads);
+  if (n == 1) return;  // a single bin has no interior edge
+  if (tid < static_cast<int>(D) && any[tid]) {  // the smoothed total, in order
+    const double* sm = smooth_of(tid);
+    double t = 0.0;
+#pragma unroll 8
+    for (std::uint32_t i = 0; i < n; ++i) t += sm[i];
+    tot[tid] = t;
+  }
+  bar_sync_n(1, nthreads);
+  for (std::uint32_t idx = tid; idx < total_el; idx += nthreads) {  // importance (grid.hpp:255-262)
+    const std::uint32_t j = idx / n, i = idx - j * n;
+    if (!any[j]) continue;
+    double* sm = smooth_of(j);
+    const double c = sm[i] / tot[j];
+    double r = 0.0;
+    if (c == 1.0) r = 1.0;
+    else if (c > 0.0) r = pow((c - 1.0) / log(c), a.alpha);
+    sm[n + i] = r;
+  }
+  bar_sync_n(1, nthreads);
+  if (tid < static_cast<int>(D) && any[tid]) {  // cumulative importance and targets, in order
+    double* sm = smooth_of(tid);
+    const double* imp = sm + n;
+    double* P = sm + 2 * n;
+    double* T = sm + 3 * n + 1;
+    double cum = 0.0;
+    P[0] = 0.0;
+    std::uint32_t k = 0;
+    for (; k + 8 <= n; k += 8) {  // loads ahead of the (possibly aliasing) stores
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = imp[k + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        cum += v[q];
+        P[k + 1 + q] = cum;
+      }
+    }
+    for (; k < n; ++k) {
+      cum += imp[k];
+      P[k + 1] = cum;
+    }
+    const double share = cum / static_cast<double>(n);
+    double target = 0.0;
+#pragma unroll 8
+    for (std::uint32_t i = 0; i + 1 < n; ++i) {
+      target += share;
+      T[i] = target;
+    }
+  }
+  bar_sync_n(1, nthreads);
+  const std::uint32_t walk_el = D * (n - 1);
+  for (std::uint32_t idx = tid; idx < walk_el; idx += nthreads) {  // the equal-share walk (grid.hpp:263-284)
+    const std::uint32_t j = idx / (n - 1), i = idx - j * (n - 1);
+    if (!any[j]) continue;
+    double* sm = smooth_of(j);
+    const double* imp = sm + n;
+    const double* P = sm + 2 * n;
+    const double t = sm[3 * n + 1 + i];
+    std::uint32_t lo_k = 0, hi_k = n - 1;
+    while (lo_k < hi_k) {
+      const std::uint32_t mid = (lo_k + hi_k) >> 1;
+      if (P[mid + 1] < t) lo_k = mid + 1;
+      else hi_k = mid;
+    }
+    std::uint32_t k = lo_k;
+    while (k + 1 < n && (imp[k] == 0.0 || P[k + 1] < t)) ++k;
+    const double* ed = edges_s + static_cast<std::size_t>(j) * n;
+    const double left = k == 0 ? lo[j] : ed[k - 1];
+    const double width = ed[k] - left;
+    sm[4 * n + i] = left + width * ((t - P[k]) / imp[k]);  // out row (after T)
+  }
+  bar_sync_n(1, nthreads);
+  for (std::uint32_t idx = tid; idx < walk_el; idx += nthreads) {  // strictly increasing?
+    const std::uint32_t j = idx / (n - 1), i = idx - j * (n - 1);
+    if (!any[j]) continue;
+    const double* out = smooth_of(j) + 4 * n;
+    const double prev = i == 0 ? lo[j] : out[i - 1];
+    const double next = i + 2 == n ? hi[j] : out[i + 1];
+    if (!(out[i] > prev) || !(out[i] < next)) bad[j] = 1;
+  }
+  bar_sync_n(1, nthreads);
+  if (tid < static_cast<int>(D) && any[tid] && bad[tid]) {  // repair passes (grid.hpp:285-294)
+    double* out = smooth_of(tid) + 4 * n;
+    double prev = lo[tid];
+    for (std::uint32_t i = 0; i + 1 < n; ++i) {
+      if (!(out[i] > prev)) out[i] = nextafter(prev, INFINITY);
+      prev = out[i];
+    }
+    double next = hi[tid];
+    for (std::uint32_t i = n - 1; i-- > 0;) {
+      if (!(out[i] < next)) out[i] = nextafter(next, -INFINITY);
+      next = out[i];
+    }
+  }
+  bar_sync_n(1, nthreads);
+  for (std::uint32_t idx = tid; idx < total_el; idx += nthreads) {
+    const std::uint32_t j = idx / n, i = idx - j * n;
+    if (!any[j]) continue;
+    a.edges[idx] = i + 1 < n ? smooth_of(j)[4 * n + i] : hi[j];
+  }
+}
+
 template <int kTag = 0>
 __global__ void adjust_grid_kernel(const AdjustArgs a) {
   extern __shared__ double adj_scratch[];
-  adjust_grid_block(a, a.contrib, adj_scratch, blockDim.x >> 5);
+  adjust_grid_block(a, a.contrib, a.edges, adj_scratch, blockDim.x >> 5);
 }
 
 #ifdef __CUDACC__
@@ -331,6 +497,7 @@ struct EpilogueArgs {
   std::uint32_t it;  ///< 1-based iteration just sampled
   int adjusting;
   int adj_warps;  ///< warps with adaptation scratch (set by launch_finish)
+  int adj_par;    ///< 1: adjust_grid_par (all axes block-wide; set by launch_finish when it fits)
   double tau, chi2max;
   AdjustArgs adj;
   int* host_flags;  ///< nullable, host-mapped: [it-1] = 1 (continue) or 2 (stop) once this iteration finished
@@ -362,19 +529,28 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   const int nbins = static_cast<int>(r.bin_axes * r.nb);
   double* contrib_out = r.contrib ? r.contrib : e.adj.contrib_scratch;
 
+  // Each accumulator is read by exactly one warp; with zero_words that warp
+  // zeroes its words right after reading them, readying the buffer for the
+  // next K1 flush off the epilogue's critical path.
+  auto zero_acc = [&](unsigned long long* w0, int naccs) {
+    __syncwarp();
+    for (int w = lane; w < naccs * kXWords; w += 32) w0[w] = 0ull;
+  };
   const int c = blockIdx.x * nwarps + warp;
   if (c < total + 2) {
     if (c == total) {
       const double v = exact::warp_round_words(r.words, r.words + kXWords);
       if (lane == 0) *r.est = v;
+      if (r.zero_words) zero_acc(r.words, 2);
     } else if (c == total + 1) {
       const double v = exact::warp_round_words(r.words + 2 * kXWords, nullptr) / r.md2;
       if (lane == 0) *r.var = v;
+      if (r.zero_words) zero_acc(r.words + 2 * kXWords, 1);
     } else {
-      const double v =
-          c < nbins ? exact::warp_round_words(r.words + static_cast<std::size_t>(kScalarAccs + c) * kXWords, nullptr)
-                    : 0.0;
+      unsigned long long* w = r.words + static_cast<std::size_t>(kScalarAccs + c) * kXWords;
+      const double v = c < nbins ? exact::warp_round_words(w, nullptr) : 0.0;
       if (lane == 0 && contrib_out) contrib_out[c] = v;
+      if (r.zero_words && c < nbins) zero_acc(w, 1);
     }
   }
   if (!with_epilogue) return;
@@ -388,10 +564,15 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   if (threadIdx.x == 0) *counter = 0u;
   if (threadIdx.x == 0) MCB_FIN_STAMP(2);
 
+  // contributions and current edges staged together (one global round trip)
   double* contrib_s = fin_smem;
-  double* scratch = fin_smem + static_cast<std::size_t>(r.dims) * r.nb;
+  double* edges_s = fin_smem + static_cast<std::size_t>(r.dims) * r.nb;
+  double* scratch = edges_s + static_cast<std::size_t>(r.dims) * r.nb;
   if (e.adjusting)
-    for (int i = threadIdx.x; i < total; i += blockDim.x) contrib_s[i] = contrib_out[i];
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      contrib_s[i] = contrib_out[i];
+      edges_s[i] = e.adj.edges[i];
+    }
   __syncthreads();
 
   RunState* st = e.st;
@@ -405,20 +586,14 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
     return;
   }
   if (threadIdx.x == 0) MCB_FIN_STAMP(3);
-  // every block has read its words: ready the buffer for the next K1 flush, on the
-  // warps the adaptation leaves idle (all threads afterwards if none is idle)
-  const int nzero = (kScalarAccs + nbins) * kXWords;
-  const int busy = 32 * (e.adjusting ? e.adj_warps : 1);
-  if (r.zero_words && busy < static_cast<int>(blockDim.x) && static_cast<int>(threadIdx.x) >= busy)
-    for (int i = threadIdx.x - busy; i < nzero; i += blockDim.x - busy) r.words[i] = 0ull;
-  if (e.adjusting) adjust_grid_block(e.adj, contrib_s, scratch, e.adj_warps);
-  if (r.zero_words && busy >= static_cast<int>(blockDim.x))
-    for (int i = threadIdx.x; i < nzero; i += blockDim.x) r.words[i] = 0ull;
-  if (threadIdx.x == 0) MCB_FIN_STAMP(4);
-  if (threadIdx.x < 32) {
+  // The weighted estimate and the convergence gate need only the history, so
+  // they run on a warp the adaptation leaves idle, concurrently with it
+  // (after it on warp 0 when every warp adapts, or in symmetric mode whose
+  // replication step is block-wide).
+  auto estimate = [&] {
     double mean, sigma, chi2;
     weighted_estimate_warp(e.hist_est, e.hist_var, e.it, mean, sigma, chi2);
-    if (threadIdx.x != 0) return;
+    if (lane != 0) return;
     st->estimate = mean;
     st->sigma = sigma;
     st->chi2_dof = chi2;
@@ -429,7 +604,18 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
     }
     if (e.host_flags) e.host_flags[e.it - 1] = st->stop ? 2 : 1;
     MCB_FIN_STAMP(5);
+  };
+  const bool par = e.adjusting && e.adj_par;
+  const bool concurrent = !e.adjusting || par || (e.adj_warps < nwarps && !e.adj.symmetric);
+  const int est_warp = e.adjusting ? nwarps - 1 : 0;
+  if (concurrent && warp == est_warp) {
+    estimate();
+    return;
   }
+  if (par) adjust_grid_par(e.adj, contrib_s, edges_s, scratch, (nwarps - 1) * 32);
+  else if (e.adjusting) adjust_grid_block(e.adj, contrib_s, edges_s, scratch, e.adj_warps);
+  if (threadIdx.x == 0) MCB_FIN_STAMP(4);
+  if (!concurrent && warp == 0) estimate();
 }
 
 // ------------------------------------------------------------------ run setup / collect

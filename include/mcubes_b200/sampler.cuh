@@ -328,11 +328,26 @@ struct CubeWalk {
   }
 };
 
+#ifdef MCB_K1_TIMING
+// latency probe (tools/latbench.cu): %globaltimer at K1's phases, min/max over blocks
+__device__ unsigned long long g_k1_times[8];
+#define MCB_K1_STAMP(i, op)                                  \
+  if (threadIdx.x == 0) {                                    \
+    unsigned long long t_;                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));   \
+    op(&g_k1_times[i], t_);                                  \
+  }
+#else
+#define MCB_K1_STAMP(i, op)
+#endif
+
 /// K1.  NB = n_bins when known at compile time (50, the reference default
 /// and every BASELINE config), 0 = runtime n_bins.
 template <class F, int D, RngKind R, int NB = 0>
 __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const SampleArgs a, const F f) {
   pdl_trigger();  // the finish kernel may launch now; it waits for this grid to complete
+  MCB_K1_STAMP(0, atomicMin)
+  MCB_K1_STAMP(1, atomicMax)
   extern __shared__ __align__(16) unsigned char smem[];
   // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
   const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (R == RngKind::philox ? 1u : 0u);
@@ -352,6 +367,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     else stage_grid_fast<D>(LW, a);
   }
   __syncthreads();
+  MCB_K1_STAMP(2, atomicMax)
 
   const int lane = tid & 31;
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
@@ -476,7 +492,9 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       coord(0);
     }
   }
+  MCB_K1_STAMP(3, atomicMin)
   __syncthreads();
+  MCB_K1_STAMP(4, atomicMax)
 
   // Flush: the block's nonzero words go straight into the exchange buffer as
   // exact 64-bit integer adds -- a few thousand per block per iteration,
@@ -505,6 +523,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       if (sum) atomicAdd(a.words + i, sum);
     }
   }
+  MCB_K1_STAMP(5, atomicMax)
 }
 
 /// Recompute one sample (cube t, sample k) -- used to report the point of a

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "mcubes_b200/mcubes.cuh"
@@ -25,7 +26,7 @@ static int fixed_cost() {
     cfg.ita = its;
     cfg.tau_rel = 1e-15;
     cfg.rng = gpu::RngKind::philox;
-    (void)gpu::integrate_ops(ctx, ops, cfg);
+    const IntegrationResult res0 = gpu::integrate_ops(ctx, ops, cfg);
     double best = 1e30;
     for (int r = 0; r < 7; ++r) {
       ctx.sync();
@@ -33,7 +34,9 @@ static int fixed_cost() {
       (void)gpu::integrate_ops(ctx, ops, cfg);
       best = std::min(best, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
-    std::printf("C++ integrate_ops itmax=%u: %.1f us\n", its, best * 1e6);
+    std::uint64_t eb;
+    std::memcpy(&eb, &res0.estimate, 8);
+    std::printf("C++ integrate_ops itmax=%u: %.1f us  (estimate bits %016llx)\n", its, best * 1e6, (unsigned long long)eb);
   }
   return 0;
 }
@@ -141,6 +144,19 @@ int main(int argc, char** argv) {
     {
       unsigned long long z[16] = {};
       cudaMemcpyToSymbol(gpu::g_fin_times, z, sizeof z);
+    }
+#endif
+#ifdef MCB_K1_TIMING
+    if (it == 20) {
+      unsigned long long tt[8];
+      cudaMemcpyFromSymbol(tt, gpu::g_k1_times, sizeof tt);
+      auto us = [&](int i) { return (double)(tt[i] - tt[0]) * 1e-3; };
+      std::printf("K1 phases (us from first block start): last block start %.2f  prologue done %.2f  first thread done %.2f  "
+                  "last block loop done %.2f  flushed %.2f\n", us(1), us(2), us(3), us(4), us(5));
+    }
+    {
+      unsigned long long z[8] = {~0ull, 0, 0, ~0ull, 0, 0, 0, 0};
+      cudaMemcpyToSymbol(gpu::g_k1_times, z, sizeof z);
     }
 #endif
     if (it > 10) {
