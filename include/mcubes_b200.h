@@ -59,7 +59,8 @@ enum mcb_integrand_id {
   MCB_T_X0SQ_HALF = 34,  /* x[0]*x[0] + 0.5                               */
   MCB_T_INF_X0POS = 35,  /* x[0] > 0 ? inf : 1                            */
   MCB_T_INF = 36,        /* inf                                           */
-  MCB_T_ZERO = 37        /* 0                                             */
+  MCB_T_ZERO = 37,       /* 0                                             */
+  MCB_T_INF_NEAR_ORIGIN = 38 /* inf if every x_j < params[0], else 1 (multi-rank failure tests) */
 };
 
 enum mcb_bin_update { MCB_BIN_ALL_AXES = 0, MCB_BIN_AXIS0_ONLY = 1, /* sampler.hpp:51-54 */
@@ -196,7 +197,10 @@ int mcb_integrate_resume(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config*
  * across ranks, then every rank finishes the iteration identically. ---- */
 int mcb_run_create(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, mcb_run** out);
 int mcb_run_destroy(mcb_run* run);
-/* Exchange buffer length (u64 words) for iteration it (1-based). */
+/* Exchange buffer length (u64 words) for iteration it (1-based; 0 = the
+ * largest).  Word 0 counts non-finite samples, then MCB_XWORDS words per
+ * accumulator (est+, est-, var, bins); all-reducing the first
+ * mcb_run_exchange_words(run, it) words covers iteration it. */
 uint64_t mcb_run_exchange_words(const mcb_run* run, uint32_t it);
 /* Use a caller-owned DEVICE buffer (>= max exchange words) for the exchange. */
 int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
@@ -207,6 +211,14 @@ int mcb_run_set_exchange(mcb_run* run, void* device_ptr);
  * turns reporting off.  (No reference counterpart: the reference's integrate
  * loop is synchronous, driver.hpp:227-256.) */
 int mcb_run_set_progress(mcb_run* run, int* host_flags);
+/* Multi-rank failure reporting: *failed = 1 if the run stopped on a
+ * non-finite sample (in any rank's slice: the count is exchanged with the
+ * words), *key = this rank's first failing sample t*p+k (all ones if none was
+ * in its slice).  Drivers all-reduce the key with MIN and hand it back with
+ * mcb_run_set_failure_key before mcb_run_result, so every rank returns the
+ * same MCB_ENONFINITE point. */
+int mcb_run_failure_key(mcb_run* run, int* failed, uint64_t* key);
+int mcb_run_set_failure_key(mcb_run* run, uint64_t key);
 /* Resume a stepped run from a checkpoint (see mcb_integrate_resume); on
  * success *next_iteration is the first iteration to sample. */
 int mcb_run_resume(mcb_run* run, const double* edges, const mcb_iteration* done, uint32_t n_done,

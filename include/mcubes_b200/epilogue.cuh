@@ -479,7 +479,7 @@ MCB_HD bool converged_dev(double est, double sigma, double chi2, double tau, dou
 
 // ------------------------------------------------------------------ finish (K3b + K4)
 struct RoundArgs {
-  unsigned long long* words;  ///< [exchange_accs][kXWords]; zeroed by the epilogue when zero_words
+  unsigned long long* words;  ///< [exchange_accs][kXWords], words[-1] the non-finite count; zeroed by the epilogue when zero_words
   std::uint32_t dims, nb, bin_axes;
   double md2;        ///< double(m) * double(m)  (sampler.hpp:330-331)
   double* est;       ///< 1 double
@@ -576,7 +576,12 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   __syncthreads();
 
   RunState* st = e.st;
-  if (*e.err_key != ~0ull) {  // NonFiniteSample: abort the run (driver.hpp:231-241 propagate)
+  // words[-1] counts non-finite samples over every rank's slice (exchanged
+  // with the words), err_key holds this rank's first one
+  const unsigned long long nonfinite = r.words[-1];
+  __syncthreads();
+  if (threadIdx.x == 0 && r.zero_words) r.words[-1] = 0ull;
+  if (*e.err_key != ~0ull || nonfinite != 0) {  // NonFiniteSample: abort the run (driver.hpp:231-241 propagate)
     if (threadIdx.x == 0) {
       st->failed = 1;
       st->failed_iteration = e.it;

@@ -372,8 +372,6 @@ inline void cube_unit_point(std::uint64_t t, std::uint64_t g, std::uint32_t dims
 namespace gpu {
 
 /// One iteration on the GPU for a host grid.  bin_axes: 0 frozen, 1 axis0, d all.
-/// Optional slice [n0, n1) of the linear work index (multi-GPU partition);
-/// words_out (nullable) receives the unrounded exchange words.
 struct SampleResult {
   double est = 0, var = 0;
   std::vector<double> contrib;
@@ -390,9 +388,11 @@ inline SampleResult sample_once(Context& ctx, const IntegrandOps& ops, const Gri
   unsigned long long* err = ctx.err_key.ensure(1);
   MCB_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream()));
   const std::uint64_t root = iteration_key(seed, iteration);
-  const std::size_t nwords = static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords;
-  unsigned long long* words = ctx.words.ensure(nwords);
-  MCB_CUDA(cudaMemsetAsync(words, 0, sizeof(unsigned long long) * nwords, ctx.stream()));
+  // exchange buffer: the non-finite count word, then the accumulator words
+  const std::size_t nwords = 1 + static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords;
+  unsigned long long* xbuf = ctx.words.ensure(nwords);
+  MCB_CUDA(cudaMemsetAsync(xbuf, 0, sizeof(unsigned long long) * nwords, ctx.stream()));
+  unsigned long long* words = xbuf + 1;
   (void)ops.k1(ctx, sh, bin_axes, root, 0, m, nullptr, err, words);  // K1 flushes straight into the words
   double* sc = ctx.scalars.ensure(2);
   double* contrib = bin_axes ? ctx.contrib.ensure(n) : nullptr;
@@ -604,7 +604,8 @@ class Run {
     ctx_.hist_var.ensure(cfg_.itmax);
     ctx_.state.ensure(1);
     ctx_.err_key.ensure(1);
-    words_ = ctx_.words.ensure(exchange_words(cfg_.dims));
+    xbuf_ = ctx_.words.ensure(exchange_words(cfg_.dims));
+    words_ = xbuf_ + 1;
     if (sizeof(double) * (n + 2 * cfg_.dims) <= Context::kPinnedBytes) {
       // one launch: the kernel reads the staged grid from pinned host memory
       // and zeroes the state and the exchange words
@@ -617,7 +618,7 @@ class Run {
       launch_pdl(run_init_kernel<0>, std::max<std::uint32_t>(1, (nw + 255) / 256), 256, 0, ctx_.stream(),
                  static_cast<const double*>(pin), static_cast<std::uint32_t>(n), cfg_.dims, ctx_.edges.ensure(n),
                  ctx_.lower.ensure(cfg_.dims), ctx_.upper.ensure(cfg_.dims), ctx_.state.get(), ctx_.err_key.get(),
-                 words_, nw);
+                 xbuf_, nw);
       ++ctx_.launches;
       ctx_.staging_recorded();
       words_clean_ = true;
@@ -674,32 +675,35 @@ class Run {
     if (it > cfg_.ita) return 0;
     return cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims;
   }
-  /// Exchange buffer length (u64 words) for the largest (adjusting) iteration.
+  /// Exchange buffer length (u64 words): one word counting non-finite samples
+  /// (so every rank learns of a failure in any rank's slice), then the
+  /// accumulators.  An all-reduce of the first exchange_words_for(it) words
+  /// covers iteration it.
   std::size_t exchange_words(std::uint32_t) const {
-    return static_cast<std::size_t>(exchange_accs(cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims, cfg_.n_bins)) *
-           kXWords;
+    return 1 + static_cast<std::size_t>(exchange_accs(cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims,
+                                                      cfg_.n_bins)) * kXWords;
   }
   std::size_t exchange_words_for(std::uint32_t it) const {
-    return static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
+    return 1 + static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
   }
-  unsigned long long* exchange() const { return words_; }
+  unsigned long long* exchange() const { return xbuf_; }
   void zero_exchange() {
-    MCB_CUDA(cudaMemsetAsync(words_, 0, sizeof(unsigned long long) * exchange_words(cfg_.dims), ctx_.stream()));
+    MCB_CUDA(cudaMemsetAsync(xbuf_, 0, sizeof(unsigned long long) * exchange_words(cfg_.dims), ctx_.stream()));
     words_clean_ = true;
   }
   /// Have finish() report per-iteration progress into host-mapped flags
   /// (Context::host_flags layout); nullptr turns it off.
   void set_host_flags(int* f) { host_flags_ = f; }
-  /// Use a caller-owned exchange buffer (e.g. a torch tensor the caller all-reduces).
-  /// Use a caller-owned exchange buffer (it is zeroed here; finish() leaves it
-  /// zeroed for the next iteration's reduce()).
+  /// Use a caller-owned exchange buffer of exchange_words() u64 (e.g. a torch
+  /// tensor the caller all-reduces).  It is zeroed here; finish() leaves it
+  /// zeroed for the next iteration.
   void set_exchange(unsigned long long* p) {
-    words_ = p ? p : ctx_.words.get();
+    xbuf_ = p ? p : ctx_.words.get();
+    words_ = xbuf_ + 1;
     zero_exchange();
   }
   const int* stop_flag() const { return &ctx_.state.get()->stop; }
 
-  /// K1 over the work slice [n0, n1) of the linear work index (default: all cubes).
   /// K1 over the work slice [n0, n1) of the linear work index (default: all
   /// cubes).  Its blocks flush straight into exchange(): after sample() the
   /// exchange words hold this slice's sums (the words are zeroed first unless
@@ -750,6 +754,22 @@ class Run {
     MCB_CUDA(cudaMemcpyAsync(&st, ctx_.state.get(), sizeof st, cudaMemcpyDeviceToHost, ctx_.stream()));
     ctx_.sync();
     return st;
+  }
+
+  /// Whether the run stopped on a non-finite sample, and this rank's first
+  /// failing sample key (t * p + k; all-ones when the failure was in another
+  /// rank's slice).  Multi-rank drivers take the minimum over ranks and hand
+  /// it back with set_failure_key() so that every rank reports the same
+  /// NonFiniteSample (the reference reports the first in serial order).
+  bool failure_key(unsigned long long& key) {
+    const RunState st = state();
+    MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
+    ctx_.sync();
+    return st.failed != 0;
+  }
+  void set_failure_key(unsigned long long key) {
+    MCB_CUDA(cudaMemcpyAsync(ctx_.err_key.get(), &key, sizeof key, cudaMemcpyHostToDevice, ctx_.stream()));
+    ctx_.sync();
   }
 
   /// Replace the device grid with host edges (dims*n_bins), stream-ordered.
@@ -823,7 +843,8 @@ class Run {
   RunConfig cfg_;
   SetupParams sp_{};
   Shape sh_{};
-  unsigned long long* words_ = nullptr;
+  unsigned long long* xbuf_ = nullptr;   ///< exchange buffer: [non-finite count][accumulator words]
+  unsigned long long* words_ = nullptr;  ///< xbuf_ + 1
   Launch last_{};
   std::uint32_t last_it_ = 0;
   int* host_flags_ = nullptr;

@@ -70,7 +70,8 @@ struct SampleArgs {
   std::uint64_t R;                      ///< rows m / g
   std::uint64_t stepR;                  ///< row mode: (T*A) mod R, A = A' = 1 + g + ... + g^(D-2)
   std::uint32_t round_keys[20];         ///< philox: (k0, k1) of rounds 0..9 (uniform; folded into LOP3)
-  unsigned long long* words;  ///< exchange buffer (zeroed): every block adds its nonzero words here
+  unsigned long long* words;  ///< exchange accumulators (zeroed): every block adds its nonzero words here;
+                              ///< words[-1] counts non-finite samples
   std::uint32_t nb_out;       ///< n_bins of the exchange layout (the padding cell folds into bin nb_out-1)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point<F, D, NB>(a, f, LW, cd, croot, k, x, bin, fx);
         if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+          atomicAdd(a.words - 1, 1ull);  // the exchanged non-finite count (all ranks stop together)
           continue;
         }
         sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
@@ -466,6 +468,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point_fast<F, D, NB>(a, f, LW, cw.dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
+          atomicAdd(a.words - 1, 1ull);  // the exchanged non-finite count (all ranks stop together)
           continue;
         }
         sum = __dadd_rn(sum, fj);

@@ -215,6 +215,12 @@ static double eval_fn(const orc_fn* f, const double* x) {
     case 35: return x[0] > 0.0 ? INFINITY : 1.0;
     case 36: return INFINITY;
     case 37: return 0.0;
+    case 38: {  /* inf_near_origin: +inf if every x_j < c (a failure inside one corner cube) */
+      const double c = f->nparams ? f->params[0] : 0.0;
+      for (uint32_t j = 0; j < d; ++j)
+        if (!(x[j] < c)) return 1.0;
+      return INFINITY;
+    }
   }
   return NAN;
 }

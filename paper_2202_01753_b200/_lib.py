@@ -87,6 +87,8 @@ SIGNATURES = {
     "mcb_run_exchange_words": (_U64, [_VP, _U32]),
     "mcb_run_set_exchange": (C.c_int, [_VP, _VP]),
     "mcb_run_set_progress": (C.c_int, [_VP, _VP]),
+    "mcb_run_failure_key": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(_U64)]),
+    "mcb_run_set_failure_key": (C.c_int, [_VP, _U64]),
     "mcb_run_resume": (C.c_int, [_VP, _PD, C.POINTER(mcb_iteration), _U32, C.POINTER(_U32)]),
     "mcb_run_exchange_ptr": (_VP, [_VP]),
     "mcb_run_work_items": (_U64, [_VP]),

@@ -85,6 +85,7 @@ IntegrandOps builtin_ops(Context& ctx, DevBuf<double>& pbuf, const mcb_integrand
       return abi::ops_Table(f->id, rng, a);
     }
     case MCB_T_X0: case MCB_T_CONST: case MCB_T_X0SQ_HALF: case MCB_T_INF_X0POS: case MCB_T_INF: case MCB_T_ZERO:
+    case MCB_T_INF_NEAR_ORIGIN:
       if (rng != RngKind::compat) throw std::invalid_argument("test integrands support the compat stream only");
       if (dims > 10) throw std::invalid_argument("test integrands are compiled for dims <= 10");
       return abi::ops_Tests(f->id, rng, a);
@@ -377,6 +378,24 @@ int mcb_run_set_progress(mcb_run* r, int* host_flags) {
   if (!r) return MCB_EINVAL;
   r->run->set_host_flags(host_flags);
   return MCB_OK;
+}
+
+int mcb_run_failure_key(mcb_run* r, int* failed, uint64_t* key) {
+  if (!r || !failed || !key) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    r->owner->ctx->activate();
+    unsigned long long k = ~0ull;
+    *failed = r->run->failure_key(k) ? 1 : 0;
+    *key = k;
+  });
+}
+
+int mcb_run_set_failure_key(mcb_run* r, uint64_t key) {
+  if (!r) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    r->owner->ctx->activate();
+    r->run->set_failure_key(key);
+  });
 }
 
 uint64_t mcb_run_work_items(const mcb_run* r) { return r ? r->run->params().m : 0; }

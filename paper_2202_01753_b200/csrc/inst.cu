@@ -47,6 +47,7 @@ IntegrandOps ops_Tests(int id, RngKind, const BuiltinArgs& a) {
     case 34: return make_ops(fn::X0SqHalf{});
     case 35: return make_ops(fn::InfIfX0Pos{});
     case 36: return make_ops(fn::Inf{});
+    case 38: return make_ops(fn::InfNearOrigin{a.n_params ? a.host_params[0] : 0.0});
     default: return make_ops(fn::Zero{});
   }
 }

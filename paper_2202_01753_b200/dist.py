@@ -75,6 +75,16 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
                 if r.iterations_used < it:
                     break
                 observer(it, r, run.grid())
-        res = run.result()
-    run.close()
+        # A non-finite sample in any rank's slice stops every rank at the same
+        # iteration (its count is exchanged with the words); report the first
+        # one in serial order over all slices, as a single process would.
+        failed, key = run.failure_key()
+        if failed:
+            k = torch.tensor([key - (1 << 63)], dtype=torch.int64, device=dev)  # u64 order in int64
+            dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
+            run.set_failure_key(int(k.item()) + (1 << 63))
+        try:
+            res = run.result()
+        finally:
+            run.close()
     return res

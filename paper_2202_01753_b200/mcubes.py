@@ -262,14 +262,16 @@ def make_table_integrand(tables, lower, upper, name: str = "table") -> Integrand
     return IntegrandSpec(name, d, lower, upper, 9, params, ref)
 
 
-_TEST_IDS = {"x0": 32, "const": 33, "x0sq_half": 34, "inf_if_x0_pos": 35, "inf": 36, "zero": 37}
+_TEST_IDS = {"x0": 32, "const": 33, "x0sq_half": 34, "inf_if_x0_pos": 35, "inf": 36, "zero": 37,
+             "inf_near_origin": 38}
 
 
 def test_integrand(kind: str, dims: int, value: float = 0.0, lower=None, upper=None) -> IntegrandSpec:
     """The small functors of the reference's unit tests (test_oracle.cpp,
     test_sampler.cpp, test_driver.cpp): x0, const, x0sq_half, inf_if_x0_pos,
-    inf, zero."""
-    params = np.array([value]) if kind == "const" else None
+    inf, zero; plus inf_near_origin (+inf if every x_j < value) for the
+    multi-rank failure path."""
+    params = np.array([value]) if kind in ("const", "inf_near_origin") else None
     lower = [0.0] * dims if lower is None else list(lower)
     upper = [1.0] * dims if upper is None else list(upper)
     return IntegrandSpec(kind, dims, lower, upper, _TEST_IDS[kind], params, None)
@@ -819,6 +821,17 @@ class Run:
         nxt = C.c_uint32()
         _raise(self._lib.mcb_run_resume(self.ptr, _dptr(edges), done, len(cp.history), C.byref(nxt)), self.ctx.ptr)
         return nxt.value
+
+    def failure_key(self):
+        """(failed, key): whether the run stopped on a non-finite sample in any
+        rank's slice, and this rank's first failing sample key t*p+k (2^64-1
+        when none was in its slice)."""
+        failed, key = C.c_int(0), C.c_uint64(0)
+        _raise(self._lib.mcb_run_failure_key(self.ptr, C.byref(failed), C.byref(key)), self.ctx.ptr)
+        return bool(failed.value), int(key.value)
+
+    def set_failure_key(self, key: int):
+        _raise(self._lib.mcb_run_set_failure_key(self.ptr, key), self.ctx.ptr)
 
     def set_progress(self, host_ptr: int):
         """Host-mapped progress flags (mcb_run_set_progress): pinned int32[itmax], zeroed."""

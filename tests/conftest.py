@@ -58,10 +58,15 @@ def ctx():
 
 def words_value(words) -> list:
     """Exact integers denoted by an exchange buffer ([accumulator][MCB_XWORDS]
-    radix-2^32 digit sums).  Different partitions carry between words at
-    different points, so compare VALUES, not word vectors."""
-    a = np.asarray(words).astype(np.uint64).reshape(-1, 67)
+    radix-2^32 digit sums, after the leading non-finite count word of a run's
+    buffer).  Different partitions carry between words at different points,
+    so compare VALUES, not word vectors."""
+    a = np.asarray(words).astype(np.uint64)
     out = []
+    if a.size % 67 == 1:  # a run's exchange buffer: [non-finite count][accumulators]
+        out.append(int(a[0]))
+        a = a[1:]
+    a = a.reshape(-1, 67)
     for row in a:
         v = 0
         for i in range(66, -1, -1):

@@ -83,3 +83,52 @@ def test_multi_rank_integrate_matches_single(world, early, ctx):
         assert conv == want.converged and used == want.iterations_used
         assert est == want.estimate and sigma == want.sigma and chi2 == want.chi2_dof
         assert he == [h.estimate for h in want.history] and hv == [h.variance for h in want.history]
+
+
+def _nf_cfg(M):
+    # 2D, g = 70: inf_near_origin(0.014) fails only inside corner cube 0, which
+    # lies in rank 0's slice (n = 0 maps to cube 0); the other ranks see no failure
+    return M.RunConfig(dims=2, maxcalls=10 ** 4, itmax=4, ita=2, tau_rel=1e-15, seed=5, lower=[0.0] * 2,
+                       upper=[1.0] * 2)
+
+
+def _nf_rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2202_01753_b200 as M
+        from paper_2202_01753_b200 import dist as mdist
+
+        torch.cuda.set_device(0)
+        try:
+            mdist.integrate(M.test_integrand("inf_near_origin", 2, 0.014), _nf_cfg(M))
+            q.put((rank, None, None))
+        except M.NonFiniteSample as e:
+            q.put((rank, e.point(), e.value()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nonfinite_in_one_rank_stops_every_rank(ctx):
+    """A non-finite sample in one rank's slice: every rank stops at the same
+    iteration (the failure count travels with the exchange words) and raises
+    the same NonFiniteSample as the single-process run (the first failing
+    sample in serial order, min-reduced over the ranks)."""
+    import paper_2202_01753_b200 as M
+
+    with pytest.raises(M.NonFiniteSample) as ei:
+        M.integrate(M.test_integrand("inf_near_origin", 2, 0.014), _nf_cfg(M), ctx=ctx)
+    want = (ei.value.point(), ei.value.value())
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    world = 2
+    procs = [mpc.Process(target=_nf_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, point, value in res:
+        assert (point, value) == want

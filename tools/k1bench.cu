@@ -49,13 +49,13 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a1);
     float best = 1e30f;
     const int between = std::getenv("K1_BETWEEN") ? std::atoi(std::getenv("K1_BETWEEN")) : 0;
-    const std::size_t nwords = static_cast<std::size_t>(gpu::exchange_accs(D, 50)) * gpu::kXWords;
-    unsigned long long* words = ctx.words.ensure(nwords);
+    const std::size_t nwords = 1 + static_cast<std::size_t>(gpu::exchange_accs(D, 50)) * gpu::kXWords;
+    unsigned long long* words = ctx.words.ensure(nwords) + 1;  // [non-finite count][accumulators]
     for (int r = 0; r < reps + 1; ++r) {
       cudaEventRecord(a0, ctx.stream());
       (void)ops.k1(ctx, sh, frozen ? 0u : D, key, 0, sh.m, nullptr, err, words);
       cudaEventRecord(a1, ctx.stream());
-      if (between == 1) cudaMemsetAsync(words, 0, sizeof(unsigned long long) * nwords, ctx.stream());
+      if (between == 1) cudaMemsetAsync(words - 1, 0, sizeof(unsigned long long) * nwords, ctx.stream());
       cudaEventSynchronize(a1);
       if (between == 2) usleep(200000);
       float ms;
@@ -94,14 +94,14 @@ int main(int argc, char** argv) {
   {  // the same kernel launched directly (no stop flag) on the run's current grid
     unsigned long long* err = ctx.err_key.ensure(1);
     cudaEventRecord(e0, ctx.stream());
-    ops.k1(ctx, run.shape(), frozen ? 0u : D, gpu::iteration_key(cfg.seed, 1), 0, run.shape().m, nullptr, err, run.exchange());
+    ops.k1(ctx, run.shape(), frozen ? 0u : D, gpu::iteration_key(cfg.seed, 1), 0, run.shape().m, nullptr, err, run.exchange() + 1);
     cudaEventRecord(e1, ctx.stream());
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     std::printf("  direct-after-run k1_ms=%.3f\n", ms);
     cudaEventRecord(e0, ctx.stream());
-    ops.k1(ctx, run.shape(), frozen ? 0u : D, gpu::iteration_key(cfg.seed, 1), 0, run.shape().m, run.stop_flag(), err, run.exchange());
+    ops.k1(ctx, run.shape(), frozen ? 0u : D, gpu::iteration_key(cfg.seed, 1), 0, run.shape().m, run.stop_flag(), err, run.exchange() + 1);
     cudaEventRecord(e1, ctx.stream());
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
