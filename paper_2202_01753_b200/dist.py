@@ -67,7 +67,9 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
                     break
             run.sample(it, n0, n1)
             run.reduce(it)
-            dist.all_reduce(xbuf, group=group)  # exact integer sum across ranks
+            # exact integer sum across ranks, of the words this iteration uses
+            # (frozen iterations: the count word and est+/est-/var only)
+            dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
             run.finish(it)
             events[it % (ahead + 1)].record(stream)
             if observer is not None:
