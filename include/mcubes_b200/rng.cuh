@@ -20,10 +20,32 @@ namespace mcubes::gpu::rng {
 
 inline constexpr std::uint64_t kGamma = 0x9e3779b97f4a7c15ull;
 
+/// z * C mod 2^64.  On the device as one IMAD.WIDE.U32 and two IMAD into its
+/// high word (the compiler's own lowering spends a fourth instruction on
+/// adding the cross products separately).
+template <std::uint64_t C>
+MCB_HD std::uint64_t mul_const(std::uint64_t z) {
+#if defined(__CUDA_ARCH__)
+  std::uint64_t r;
+  asm("{\n\t.reg .u32 zl, zh, rl, rh;\n\t"
+      "mov.b64 {zl, zh}, %1;\n\t"
+      "mul.wide.u32 %0, zl, %2;\n\t"
+      "mov.b64 {rl, rh}, %0;\n\t"
+      "mad.lo.u32 rh, zh, %2, rh;\n\t"
+      "mad.lo.u32 rh, zl, %3, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t}"
+      : "=l"(r)
+      : "l"(z), "n"(static_cast<std::uint32_t>(C)), "n"(static_cast<std::uint32_t>(C >> 32)));
+  return r;
+#else
+  return z * C;
+#endif
+}
+
 /// SplitMix64 finalizer (rng.hpp:29-33).
 MCB_HD std::uint64_t avalanche(std::uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z = mul_const<0xbf58476d1ce4e5b9ull>(z ^ (z >> 30));
+  z = mul_const<0x94d049bb133111ebull>(z ^ (z >> 27));
   return z ^ (z >> 31);
 }
 
