@@ -218,6 +218,25 @@ int mcb_run_set_progress(mcb_run* run, int* host_flags);
  * mcb_run_set_failure_key before mcb_run_result, so every rank returns the
  * same MCB_ENONFINITE point. */
 int mcb_run_failure_key(mcb_run* run, int* failed, uint64_t* key);
+
+/* ---- multi-GPU exchange over peer memory (NVLink / NVSwitch) instead of a
+ * collective.  Every rank allocates two exchange buffers (odd and even
+ * iterations, mcb_run_exchange_words(run, 0) u64 each), a flag array
+ * (npeers u64) and a block counter (u32) with mcb_dev_alloc (zeroed), shares
+ * their CUDA IPC handles (mcb_ipc_handle / mcb_ipc_open) and hands every
+ * rank's pointers to mcb_run_set_peers.  Each iteration is then
+ * mcb_run_sample + mcb_run_finish with no collective: K1's blocks add their
+ * exact words into every rank's buffer with system-scope reductions and
+ * release a per-iteration flag; the finish kernel acquires all ranks' flags.
+ * Arrays are indexed by rank; npeers <= 8; 0 turns it off. ---- */
+#define MCB_IPC_HANDLE_BYTES 64
+int mcb_run_set_peers(mcb_run* run, int rank, int npeers, void* const* bufs_odd, void* const* bufs_even,
+                      void* const* flags, void* counter);
+int mcb_dev_alloc(mcb_ctx* ctx, uint64_t bytes, void** ptr);
+int mcb_dev_free(mcb_ctx* ctx, void* ptr);
+int mcb_ipc_handle(mcb_ctx* ctx, void* ptr, unsigned char* handle);
+int mcb_ipc_open(mcb_ctx* ctx, const unsigned char* handle, void** ptr);
+int mcb_ipc_close(mcb_ctx* ctx, void* ptr);
 int mcb_run_set_failure_key(mcb_run* run, uint64_t key);
 /* Resume a stepped run from a checkpoint (see mcb_integrate_resume); on
  * success *next_iteration is the first iteration to sample. */

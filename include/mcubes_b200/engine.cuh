@@ -202,6 +202,10 @@ class Context {
   DevBuf<unsigned long long> words, err_key;
   DevBuf<RunState> state;
   DevBuf<unsigned int> counter;  ///< finish-kernel last-block counter (self-resetting)
+  DevBuf<unsigned int> peer_counter;  ///< K1 last-block counter of the peer-memory exchange (self-resetting)
+  /// Peer-memory exchange of the launch being enqueued (npeers == 0: off);
+  /// set by Run around its K1 / finish launches.
+  PeerArgs peer{};
   DevBuf<double> table;  ///< parameters of a stateful integrand (owned copy)
 
   static constexpr std::size_t kPinnedBytes = 1 << 20;
@@ -364,6 +368,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.nb_out = sh.nb;
   a.err_key = err_key;
   a.stop = stop;
+  a.peer = ctx.peer;
   launch_pdl(kern, L.blocks, kThreads, L.smem, ctx.stream(), a, f);
   ++ctx.launches;
   return L;
@@ -468,6 +473,11 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   r.contrib = contrib;
   r.stop = stop;
   r.zero_words = (zero_words && epi) ? 1 : 0;
+  if (epi && ctx.peer.npeers) {
+    r.wait_flags = ctx.peer.my_flags;
+    r.nwait = ctx.peer.npeers;
+    r.wait_value = ctx.peer.flag;
+  }
   EpilogueArgs e{};
   std::size_t smem = 0;
   if (epi) {

@@ -487,6 +487,9 @@ struct RoundArgs {
   double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
   const int* stop;
   int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K1 flush (integrate loop)
+  const unsigned long long* wait_flags;  ///< peer-memory exchange: wait until these nwait flags reach wait_value
+  int nwait;
+  unsigned long long wait_value;
 };
 
 struct EpilogueArgs {
@@ -524,6 +527,12 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   const int stop0 = r.stop ? *r.stop : 0;
   __syncthreads();  // every thread reads `stop` before the last block may set it
   if (stop0) return;
+  if (r.nwait) {  // peer-memory exchange: every rank's K1 has added its words into ours
+    if (threadIdx.x == 0)
+      for (int q = 0; q < r.nwait; ++q)
+        while (ld_acquire_sys(r.wait_flags + q) < r.wait_value) __nanosleep(64);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int total = static_cast<int>(r.dims * r.nb);
   const int nbins = static_cast<int>(r.bin_axes * r.nb);

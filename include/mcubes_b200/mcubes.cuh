@@ -710,11 +710,42 @@ class Run {
   /// finish() already left them zero).
   void sample(std::uint32_t it, std::uint64_t n0 = 0, std::uint64_t n1 = ~0ull) {
     if (n1 > sh_.m) n1 = sh_.m;
+    if (npeers_) {
+      // peer-memory exchange: never zero here -- other ranks may already be
+      // adding this iteration's words into our buffer; finish() leaves each
+      // buffer zeroed after reading it, and the two alternate by parity
+      use_peers(it);
+      last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(),
+                      ctx_.err_key.get(), words_);
+      ctx_.peer.npeers = 0;
+      last_it_ = it;
+      return;
+    }
     if (!words_clean_) zero_exchange();
     last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get(),
                     words_);
     words_clean_ = false;
     last_it_ = it;
+  }
+
+  /// Multi-GPU exchange over peer memory instead of a collective: rank
+  /// `rank` of `npeers`; bufs[0] / bufs[1] hold every rank's exchange buffer
+  /// (exchange_words() u64 each, zeroed) for odd / even iterations, flags
+  /// every rank's flag array (npeers u64, zeroed), counter this rank's K1
+  /// block counter (u32, zeroed).  Device pointers, already mapped into this
+  /// process (CUDA IPC).  npeers = 0 turns it off.
+  void set_peers(int rank, int npeers, unsigned long long* const* bufs_odd, unsigned long long* const* bufs_even,
+                 unsigned long long* const* flags, unsigned int* counter) {
+    if (npeers < 0 || npeers > kMaxPeers || (npeers && (rank < 0 || rank >= npeers)))
+      throw std::invalid_argument("set_peers: need 0 <= rank < npeers <= 8");
+    npeers_ = npeers;
+    rank_ = rank;
+    for (int q = 0; q < npeers; ++q) {
+      peer_bufs_[1][q] = bufs_odd[q];
+      peer_bufs_[0][q] = bufs_even[q];
+      peer_flags_[q] = flags[q];
+    }
+    peer_counter_ = counter;
   }
 
   /// The cross-block reduction (the reference's in-process exact merge,
@@ -728,6 +759,7 @@ class Run {
   /// K3b + K4 (one fused kernel) for iteration it, after the optional
   /// all-reduce of exchange().
   void finish(std::uint32_t it) {
+    if (npeers_) use_peers(it);
     const std::uint32_t ba = bin_axes(it);
     EpilogueArgs e{};
     e.st = ctx_.state.get();
@@ -746,6 +778,7 @@ class Run {
     e.host_flags = host_flags_;
     launch_finish(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
                   ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e, /*zero_words=*/true);
+    ctx_.peer.npeers = 0;
     words_clean_ = true;  // (or the run is stopped, and reduce() is a no-op)
   }
 
@@ -843,6 +876,27 @@ class Run {
   RunConfig cfg_;
   SetupParams sp_{};
   Shape sh_{};
+  /// Point the launch at iteration it's buffers: parity it & 1, flag = it.
+  void use_peers(std::uint32_t it) {
+    PeerArgs& p = ctx_.peer;
+    p = PeerArgs{};
+    const int par = static_cast<int>(it & 1u);
+    for (int q = 0; q < npeers_; ++q) {
+      p.words[q] = peer_bufs_[par][q] + 1;
+      p.flags[q] = peer_flags_[q] + rank_;
+    }
+    p.my_flags = peer_flags_[rank_];
+    p.counter = peer_counter_;
+    p.flag = it;
+    p.npeers = npeers_;
+    xbuf_ = peer_bufs_[par][rank_];
+    words_ = xbuf_ + 1;
+  }
+
+  int npeers_ = 0, rank_ = 0;
+  unsigned long long* peer_bufs_[2][kMaxPeers] = {};
+  unsigned long long* peer_flags_[kMaxPeers] = {};
+  unsigned int* peer_counter_ = nullptr;
   unsigned long long* xbuf_ = nullptr;   ///< exchange buffer: [non-finite count][accumulator words]
   unsigned long long* words_ = nullptr;  ///< xbuf_ + 1
   Launch last_{};

@@ -75,6 +75,7 @@ struct SampleArgs {
   std::uint32_t nb_out;       ///< n_bins of the exchange layout (the padding cell folds into bin nb_out-1)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
+  PeerArgs peer;                ///< multi-GPU exchange over peer memory (peer.npeers == 0: local words)
 };
 
 /// Accumulator slots in one block's partial.
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   MCB_K1_STAMP(0, atomicMin)
   MCB_K1_STAMP(1, atomicMax)
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int nonfinite_s;  // this block's non-finite samples (flushed with the words)
   // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
   const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (R == RngKind::philox ? 1u : 0u);
   double2* LW = reinterpret_cast<double2*>(smem);
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     const int nwords = nacc * kXWords;
     for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
     for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
+    if (tid == 0) nonfinite_s = 0u;
     pdl_wait();  // the grid, the stop flag and the exchange words come from the previous kernels
     if (a.stop && *a.stop) return;  // (uniform across the block)
     if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point<F, D, NB>(a, f, LW, cd, croot, k, x, bin, fx);
         if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-          atomicAdd(a.words - 1, 1ull);  // the exchanged non-finite count (all ranks stop together)
+          atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
           continue;
         }
         sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
@@ -468,7 +471,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point_fast<F, D, NB>(a, f, LW, cw.dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-          atomicAdd(a.words - 1, 1ull);  // the exchanged non-finite count (all ranks stop together)
+          atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
           continue;
         }
         sum = __dadd_rn(sum, fj);
@@ -506,6 +509,17 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   // back.  Integer addition is order-free: bit-reproducible for any launch
   // geometry and GPU count.  (The reference merges per-worker ExactSums in
   // worker order, sampler.hpp:272-276; the integer sum is the same.)
+  // With the peer-memory exchange every word goes to every rank's buffer
+  // (system-scope reductions over NVLink), otherwise to the local buffer
+  // that a collective then all-reduces.
+  const int npeers = a.peer.npeers;
+  auto add_word = [&](std::ptrdiff_t idx, unsigned long long v) {
+    if (npeers == 0) {
+      atomicAdd(a.words + idx, v);
+    } else {
+      for (int q = 0; q < npeers; ++q) red_add_sys(a.peer.words[q] + idx, v);
+    }
+  };
   {
     const int ncells = static_cast<int>(a.bin_axes * nb);
     for (int i = tid; i < ncells * kXWords; i += nt) {
@@ -514,7 +528,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       const int c = i / kXWords, w = i - c * kXWords;
       const int ax = c / static_cast<int>(nb), cell = c - ax * static_cast<int>(nb);
       const int slot = ax * static_cast<int>(a.nb_out) + min(cell, static_cast<int>(a.nb_out) - 1);
-      atomicAdd(a.words + static_cast<std::size_t>(kScalarAccs + slot) * kXWords + w, static_cast<unsigned long long>(v));
+      add_word(static_cast<std::ptrdiff_t>(kScalarAccs + slot) * kXWords + w, static_cast<unsigned long long>(v));
     }
     // est+/est-/var: the 32 lane copies folded into u64 word sums (< 2^37, exact)
     for (int i = tid; i < kScalarAccs * kXWords; i += nt) {
@@ -523,7 +537,20 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       unsigned long long sum = 0;
 #pragma unroll 8
       for (int l = 0; l < kLaneCopies; ++l) sum += src[l * kXWords];
-      if (sum) atomicAdd(a.words + i, sum);
+      if (sum) add_word(i, sum);
+    }
+    if (tid == 0 && nonfinite_s) add_word(-1, nonfinite_s);  // words[-1]: the non-finite count
+  }
+  if (npeers) {
+    // Publish "this rank's words are in": every thread's reductions are
+    // ordered before the block's arrival (fence.sc.sys + barrier); the last
+    // block to arrive releases the iteration's flag into every rank's slot.
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(a.peer.counter, 1u) == gridDim.x - 1) {
+      *a.peer.counter = 0u;  // ready for the next launch (stream order)
+      __threadfence_system();
+      for (int q = 0; q < npeers; ++q) st_release_sys(a.peer.flags[q], a.peer.flag);
     }
   }
   MCB_K1_STAMP(5, atomicMax)

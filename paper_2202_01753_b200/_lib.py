@@ -89,6 +89,12 @@ SIGNATURES = {
     "mcb_run_set_progress": (C.c_int, [_VP, _VP]),
     "mcb_run_failure_key": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(_U64)]),
     "mcb_run_set_failure_key": (C.c_int, [_VP, _U64]),
+    "mcb_run_set_peers": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP), _VP]),
+    "mcb_dev_alloc": (C.c_int, [_VP, _U64, C.POINTER(_VP)]),
+    "mcb_dev_free": (C.c_int, [_VP, _VP]),
+    "mcb_ipc_handle": (C.c_int, [_VP, _VP, C.c_char_p]),
+    "mcb_ipc_open": (C.c_int, [_VP, C.c_char_p, C.POINTER(_VP)]),
+    "mcb_ipc_close": (C.c_int, [_VP, _VP]),
     "mcb_run_resume": (C.c_int, [_VP, _PD, C.POINTER(mcb_iteration), _U32, C.POINTER(_U32)]),
     "mcb_run_exchange_ptr": (_VP, [_VP]),
     "mcb_run_work_items": (_U64, [_VP]),

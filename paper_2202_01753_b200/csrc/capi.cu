@@ -380,6 +380,65 @@ int mcb_run_set_progress(mcb_run* r, int* host_flags) {
   return MCB_OK;
 }
 
+int mcb_run_set_peers(mcb_run* r, int rank, int npeers, void* const* bufs_odd, void* const* bufs_even,
+                      void* const* flags, void* counter) {
+  if (!r || (npeers && (!bufs_odd || !bufs_even || !flags || !counter))) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    r->run->set_peers(rank, npeers, reinterpret_cast<unsigned long long* const*>(bufs_odd),
+                      reinterpret_cast<unsigned long long* const*>(bufs_even),
+                      reinterpret_cast<unsigned long long* const*>(flags), static_cast<unsigned int*>(counter));
+  });
+}
+
+int mcb_dev_alloc(mcb_ctx* c, uint64_t bytes, void** ptr) {
+  if (!c || !ptr || !bytes) return MCB_EINVAL;
+  return guarded(c, [&] {
+    c->ctx->activate();
+    void* p = nullptr;
+    MCB_CUDA(cudaMalloc(&p, bytes));
+    MCB_CUDA(cudaMemset(p, 0, bytes));
+    MCB_CUDA(cudaDeviceSynchronize());
+    *ptr = p;
+  });
+}
+
+int mcb_dev_free(mcb_ctx* c, void* ptr) {
+  if (!c) return MCB_EINVAL;
+  return guarded(c, [&] {
+    c->ctx->activate();
+    MCB_CUDA(cudaFree(ptr));
+  });
+}
+
+int mcb_ipc_handle(mcb_ctx* c, void* ptr, unsigned char* handle) {
+  if (!c || !ptr || !handle) return MCB_EINVAL;
+  return guarded(c, [&] {
+    c->ctx->activate();
+    cudaIpcMemHandle_t h;
+    MCB_CUDA(cudaIpcGetMemHandle(&h, ptr));
+    static_assert(sizeof h == MCB_IPC_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int mcb_ipc_open(mcb_ctx* c, const unsigned char* handle, void** ptr) {
+  if (!c || !handle || !ptr) return MCB_EINVAL;
+  return guarded(c, [&] {
+    c->ctx->activate();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    MCB_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int mcb_ipc_close(mcb_ctx* c, void* ptr) {
+  if (!c || !ptr) return MCB_EINVAL;
+  return guarded(c, [&] {
+    c->ctx->activate();
+    MCB_CUDA(cudaIpcCloseMemHandle(ptr));
+  });
+}
+
 int mcb_run_failure_key(mcb_run* r, int* failed, uint64_t* key) {
   if (!r || !failed || !key) return MCB_EINVAL;
   return guarded(r->owner, [&] {

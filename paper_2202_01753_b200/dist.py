@@ -11,6 +11,11 @@ device to bit-identical values: results are independent of the GPU count and
 equal to the single-GPU (and reference) result.  This replaces the
 reference's in-process exact merge of per-worker partials
 (sampler.hpp:272-276).
+
+transport="peer" replaces the all-reduce by the sampling kernel itself:
+its blocks add their words into every rank's buffer over peer memory (CUDA
+IPC mappings, system-scope reductions) and release a per-iteration flag that
+every rank's finish kernel acquires (PeerExchange below).
 """
 from __future__ import annotations
 
@@ -26,11 +31,88 @@ def partition(m: int, world: int, rank: int):
     return rank * m // world, (rank + 1) * m // world
 
 
+class PeerExchange:
+    """The peer-memory exchange's buffers for one run on this rank: two
+    exchange buffers (odd / even iterations), a flag array and a block
+    counter, allocated zeroed with cudaMalloc and shared with every rank of
+    the group through CUDA IPC handles (all_gather_object).  Every rank ends
+    up with every rank's device pointers (its own directly, the others'
+    mapped over NVLink)."""
+
+    def __init__(self, ctx: M.Context, words: int, group=None):
+        import ctypes as C
+        import torch.distributed as dist
+
+        from . import _lib as L
+
+        self._lib, self.ctx = L.lib(), ctx
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("peer-memory exchange: at most 8 ranks")
+        self.group = group
+        own = [self._alloc(8 * words), self._alloc(8 * words), self._alloc(8 * self.world), self._alloc(4)]
+        self.own = own
+        handles = []
+        for p in own[:3]:
+            h = C.create_string_buffer(64)
+            M._raise(self._lib.mcb_ipc_handle(ctx.ptr, C.c_void_p(p), h), ctx.ptr)
+            handles.append(h.raw)
+        every = [None] * self.world
+        dist.all_gather_object(every, handles, group=group)
+        self.opened = []
+        ptrs = []
+        for q, hs in enumerate(every):
+            if q == self.rank:
+                ptrs.append(own[:3])
+                continue
+            row = []
+            for h in hs:
+                out = C.c_void_p()
+                M._raise(self._lib.mcb_ipc_open(ctx.ptr, h, C.byref(out)), ctx.ptr)
+                self.opened.append(out.value)
+                row.append(out.value)
+            ptrs.append(row)
+        self.bufs_odd = [r[0] for r in ptrs]
+        self.bufs_even = [r[1] for r in ptrs]
+        self.flags = [r[2] for r in ptrs]
+        self.counter = own[3]
+
+    def _alloc(self, nbytes: int) -> int:
+        import ctypes as C
+
+        out = C.c_void_p()
+        M._raise(self._lib.mcb_dev_alloc(self.ctx.ptr, nbytes, C.byref(out)), self.ctx.ptr)
+        return out.value
+
+    def attach(self, run: M.Run):
+        run.set_peers(self.rank, self.world, self.bufs_odd, self.bufs_even, self.flags, self.counter)
+
+    def close(self):
+        """Collective: unmap the peers' buffers, then free ours once every
+        rank has unmapped them."""
+        import ctypes as C
+        import torch.distributed as dist
+
+        for p in self.opened:
+            self._lib.mcb_ipc_close(self.ctx.ptr, C.c_void_p(p))
+        self.opened = []
+        dist.barrier(group=self.group)
+        for p in self.own:
+            self._lib.mcb_dev_free(self.ctx.ptr, C.c_void_p(p))
+        self.own = []
+
+
 def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.Context] = None,
-              observer=None, resume: Optional[M.Checkpoint] = None) -> M.IntegrationResult:
+              observer=None, resume: Optional[M.Checkpoint] = None, transport: str = "collective") -> M.IntegrationResult:
     """integrate() across the ranks of `group` (default: WORLD).  Every rank
     returns the same IntegrationResult.  `resume` continues from a checkpoint
-    (every rank passes the same one)."""
+    (every rank passes the same one).  transport="collective" all-reduces the
+    exchange buffer through the process group (NCCL over NVLink);
+    transport="peer" has K1 write every rank's buffer directly over peer
+    memory (CUDA IPC, system-scope reductions and flags), with no collective
+    inside the iteration loop."""
+    if transport not in ("collective", "peer"):
+        raise ValueError("transport must be 'collective' or 'peer'")
     import torch
     import torch.distributed as dist
 
@@ -53,12 +135,20 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
         run = M.Run(f, cfg, ctx)
         run.set_progress(flags.data_ptr())
         n0, n1 = partition(run.work_items, world, rank)
-        xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
-        run.set_exchange(xbuf.data_ptr())
+        peers = None
+        if transport == "peer":
+            torch.cuda.current_stream(dev).synchronize()
+            peers = PeerExchange(ctx, run.exchange_words(), group)
+            peers.attach(run)
+        else:
+            xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
+            run.set_exchange(xbuf.data_ptr())
         first = run.resume(resume) if resume is not None else 1
         if first > 1 and run.result().converged:
             res = run.result()
             run.close()
+            if peers is not None:
+                peers.close()
             return res
         for it in range(first, cfg.itmax + 1):
             if observer is None and it >= first + ahead:
@@ -67,9 +157,10 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
                     break
             run.sample(it, n0, n1)
             run.reduce(it)
-            # exact integer sum across ranks, of the words this iteration uses
-            # (frozen iterations: the count word and est+/est-/var only)
-            dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
+            if peers is None:
+                # exact integer sum across ranks, of the words this iteration uses
+                # (frozen iterations: the count word and est+/est-/var only)
+                dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
             run.finish(it)
             events[it % (ahead + 1)].record(stream)
             if observer is not None:
@@ -89,4 +180,7 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
             res = run.result()
         finally:
             run.close()
+            if peers is not None:
+                torch.cuda.current_stream(dev).synchronize()
+                peers.close()
     return res

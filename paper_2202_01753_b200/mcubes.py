@@ -830,6 +830,14 @@ class Run:
         _raise(self._lib.mcb_run_failure_key(self.ptr, C.byref(failed), C.byref(key)), self.ctx.ptr)
         return bool(failed.value), int(key.value)
 
+    def set_peers(self, rank: int, npeers: int, bufs_odd, bufs_even, flags, counter: int):
+        """Peer-memory exchange (mcb_run_set_peers): per-rank device pointers
+        of the odd/even-iteration exchange buffers and flag arrays, and this
+        rank's block counter.  npeers = 0 turns it off."""
+        arr = lambda xs: (C.c_void_p * max(npeers, 1))(*[C.c_void_p(x) for x in xs])  # noqa: E731
+        _raise(self._lib.mcb_run_set_peers(self.ptr, rank, npeers, arr(bufs_odd), arr(bufs_even), arr(flags),
+                                           C.c_void_p(counter)), self.ctx.ptr)
+
     def set_failure_key(self, key: int):
         _raise(self._lib.mcb_run_set_failure_key(self.ptr, key), self.ctx.ptr)
 

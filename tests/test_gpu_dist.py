@@ -132,3 +132,92 @@ def test_nonfinite_in_one_rank_stops_every_rank(ctx):
         assert p.exitcode == 0
     for _, point, value in res:
         assert (point, value) == want
+
+
+def test_peer_exchange_virtual_ranks_match_single(ctx):
+    """The peer-memory exchange's device path (system-scope reductions into
+    every rank's buffer, release/acquire flags, odd/even buffers) with two
+    ranks in one process on one GPU: each rank's K1 writes both ranks'
+    buffers, each finish waits for both flags.  The kernels of the two ranks
+    are separated by device synchronisations (on one GPU a spinning finish
+    must not hold SMs the other rank's K1 needs)."""
+    import ctypes as C
+
+    import paper_2202_01753_b200 as M
+    from paper_2202_01753_b200 import _lib as L
+    from paper_2202_01753_b200 import dist as mdist
+
+    for early in (False, True):
+        cfg = _cfg(M, early)
+        f = M.make_suite_integrand(FAMILY[early], D)
+        want = M.integrate(f, cfg, ctx=ctx)
+        lib = L.lib()
+        ctxs = [M.Context(0), M.Context(0)]
+        runs = [M.Run(f, cfg, c) for c in ctxs]
+        words = runs[0].exchange_words()
+
+        def alloc(n):
+            out = C.c_void_p()
+            assert lib.mcb_dev_alloc(ctxs[0].ptr, n, C.byref(out)) == 0
+            return out.value
+
+        odd, even, flags, counters = [alloc(8 * words) for _ in range(2)], [alloc(8 * words) for _ in range(2)], \
+            [alloc(16) for _ in range(2)], [alloc(4) for _ in range(2)]
+        for r in range(2):
+            runs[r].set_peers(r, 2, odd, even, flags, counters[r])
+        m = runs[0].work_items
+        torch.cuda.synchronize()
+        for it in range(1, cfg.itmax + 1):
+            for r in range(2):
+                runs[r].sample(it, *mdist.partition(m, 2, r))
+            torch.cuda.synchronize()
+            for r in range(2):
+                runs[r].finish(it)
+            torch.cuda.synchronize()
+        got = [run.result() for run in runs]
+        for run in runs:
+            run.close()
+        for p in odd + even + flags + counters:
+            lib.mcb_dev_free(ctxs[0].ptr, C.c_void_p(p))
+        for g in got:
+            assert g.iterations_used == want.iterations_used and g.converged == want.converged
+            assert g.estimate == want.estimate and g.sigma == want.sigma and g.chi2_dof == want.chi2_dof
+            assert [h.estimate for h in g.history] == [h.estimate for h in want.history]
+
+
+def _peer_rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2202_01753_b200 as M
+        from paper_2202_01753_b200 import dist as mdist
+
+        torch.cuda.set_device(0)
+        r = mdist.integrate(M.make_suite_integrand(FAMILY[False], D), _cfg(M, False), transport="peer")
+        q.put((rank, r.estimate, r.sigma, r.chi2_dof, [h.estimate for h in r.history], r.iterations_used))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_two_processes(ctx):
+    """dist.integrate(transport="peer"): two processes share their exchange
+    buffers and flags through CUDA IPC (here both on cuda:0, time-sliced;
+    on an NVLink box each on its own GPU) and agree bitwise with the
+    single-process run, with no collective inside the iteration loop."""
+    import paper_2202_01753_b200 as M
+
+    want = M.integrate(M.make_suite_integrand(FAMILY[False], D), _cfg(M, False), ctx=ctx)
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_peer_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, est, sigma, chi2, he, used in res:
+        assert used == want.iterations_used
+        assert est == want.estimate and sigma == want.sigma and chi2 == want.chi2_dof
+        assert he == [h.estimate for h in want.history]
