@@ -31,58 +31,82 @@ def partition(m: int, world: int, rank: int):
     return rank * m // world, (rank + 1) * m // world
 
 
-class PeerExchange:
-    """The peer-memory exchange's buffers for one run on this rank: two
-    exchange buffers (odd / even iterations), a flag array and a block
-    counter, allocated zeroed with cudaMalloc and shared with every rank of
-    the group through CUDA IPC handles (all_gather_object).  Every rank ends
-    up with every rank's device pointers (its own directly, the others'
-    mapped over NVLink)."""
+class _CudaPeerMemory:
+    """Device allocation and CUDA IPC through the library (mcb_dev_alloc,
+    mcb_ipc_handle / mcb_ipc_open / mcb_ipc_close, mcb_dev_free)."""
 
-    def __init__(self, ctx: M.Context, words: int, group=None):
-        import ctypes as C
-        import torch.distributed as dist
-
+    def __init__(self, ctx: M.Context):
         from . import _lib as L
 
         self._lib, self.ctx = L.lib(), ctx
-        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
-        if self.world > 8:
-            raise ValueError("peer-memory exchange: at most 8 ranks")
-        self.group = group
-        own = [self._alloc(8 * words), self._alloc(8 * words), self._alloc(8 * self.world), self._alloc(4)]
-        self.own = own
-        handles = []
-        for p in own[:3]:
-            h = C.create_string_buffer(64)
-            M._raise(self._lib.mcb_ipc_handle(ctx.ptr, C.c_void_p(p), h), ctx.ptr)
-            handles.append(h.raw)
-        every = [None] * self.world
-        dist.all_gather_object(every, handles, group=group)
-        self.opened = []
-        ptrs = []
-        for q, hs in enumerate(every):
-            if q == self.rank:
-                ptrs.append(own[:3])
-                continue
-            row = []
-            for h in hs:
-                out = C.c_void_p()
-                M._raise(self._lib.mcb_ipc_open(ctx.ptr, h, C.byref(out)), ctx.ptr)
-                self.opened.append(out.value)
-                row.append(out.value)
-            ptrs.append(row)
-        self.bufs_odd = [r[0] for r in ptrs]
-        self.bufs_even = [r[1] for r in ptrs]
-        self.flags = [r[2] for r in ptrs]
-        self.counter = own[3]
 
-    def _alloc(self, nbytes: int) -> int:
+    def alloc(self, nbytes: int) -> int:
         import ctypes as C
 
         out = C.c_void_p()
         M._raise(self._lib.mcb_dev_alloc(self.ctx.ptr, nbytes, C.byref(out)), self.ctx.ptr)
         return out.value
+
+    def handle(self, ptr: int) -> bytes:
+        import ctypes as C
+
+        h = C.create_string_buffer(64)
+        M._raise(self._lib.mcb_ipc_handle(self.ctx.ptr, C.c_void_p(ptr), h), self.ctx.ptr)
+        return h.raw
+
+    def open(self, handle: bytes) -> int:
+        import ctypes as C
+
+        out = C.c_void_p()
+        M._raise(self._lib.mcb_ipc_open(self.ctx.ptr, handle, C.byref(out)), self.ctx.ptr)
+        return out.value
+
+    def close(self, ptr: int):
+        import ctypes as C
+
+        self._lib.mcb_ipc_close(self.ctx.ptr, C.c_void_p(ptr))
+
+    def free(self, ptr: int):
+        import ctypes as C
+
+        self._lib.mcb_dev_free(self.ctx.ptr, C.c_void_p(ptr))
+
+
+class PeerExchange:
+    """The peer-memory exchange's buffers for one run on this rank: two
+    exchange buffers (odd / even iterations), a flag array and a block
+    counter, allocated zeroed and shared with every rank of the group through
+    IPC handles (all_gather_object).  Every rank ends up with every rank's
+    pointers, indexed by rank: its own directly, the others' mapped (over
+    NVLink on an HGX box).  `memory` supplies alloc/handle/open/close/free
+    (the CUDA library by default; the CPU tests inject a stand-in)."""
+
+    def __init__(self, ctx: Optional[M.Context], words: int, group=None, memory=None):
+        import torch.distributed as dist
+
+        self.mem = memory if memory is not None else _CudaPeerMemory(ctx)
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("peer-memory exchange: at most 8 ranks")
+        self.group = group
+        # odd buffer, even buffer, flag array (one u64 slot per rank), block counter
+        self.own = [self.mem.alloc(8 * words), self.mem.alloc(8 * words), self.mem.alloc(8 * self.world),
+                    self.mem.alloc(4)]
+        every = [None] * self.world
+        dist.all_gather_object(every, [self.mem.handle(p) for p in self.own[:3]], group=group)
+        self.opened = []
+        table = []
+        for q, hs in enumerate(every):
+            if q == self.rank:
+                table.append(self.own[:3])
+                continue
+            row = [self.mem.open(h) for h in hs]
+            self.opened += row
+            table.append(row)
+        self.bufs_odd = [r[0] for r in table]
+        self.bufs_even = [r[1] for r in table]
+        self.flags = [r[2] for r in table]
+        self.counter = self.own[3]
 
     def attach(self, run: M.Run):
         run.set_peers(self.rank, self.world, self.bufs_odd, self.bufs_even, self.flags, self.counter)
@@ -90,15 +114,14 @@ class PeerExchange:
     def close(self):
         """Collective: unmap the peers' buffers, then free ours once every
         rank has unmapped them."""
-        import ctypes as C
         import torch.distributed as dist
 
         for p in self.opened:
-            self._lib.mcb_ipc_close(self.ctx.ptr, C.c_void_p(p))
+            self.mem.close(p)
         self.opened = []
         dist.barrier(group=self.group)
         for p in self.own:
-            self._lib.mcb_dev_free(self.ctx.ptr, C.c_void_p(p))
+            self.mem.free(p)
         self.own = []
 
 

@@ -98,3 +98,81 @@ def test_two_rank_exchange_is_exact():
     assert r["m"] == 5 ** 4 and r["p"] == 3
     assert list(r["hist_est"]) == e0 and list(r["hist_var"]) == v0
     assert [g.tobytes() for g in r["grids"]] == g0
+
+
+class _FakePeerMemory:
+    """Stand-in for the CUDA allocation / IPC calls of dist.PeerExchange: a
+    'pointer' is 1000 * (rank + 1) + index and its 'handle' encodes the same
+    number, so every rank can check the table it assembles."""
+
+    def __init__(self, rank):
+        self.rank, self.n, self.log = rank, 0, []
+
+    def alloc(self, nbytes):
+        self.n += 1
+        p = 1000 * (self.rank + 1) + self.n
+        self.log.append(("alloc", p, nbytes))
+        return p
+
+    def handle(self, ptr):
+        return ptr.to_bytes(8, "little") + bytes(56)
+
+    def open(self, handle):
+        assert len(handle) == 64
+        p = int.from_bytes(handle[:8], "little")
+        self.log.append(("open", p))
+        return p
+
+    def close(self, ptr):
+        self.log.append(("close", ptr))
+
+    def free(self, ptr):
+        self.log.append(("free", ptr))
+
+
+def _peer_table_rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_01753_b200.dist import PeerExchange
+
+        mem = _FakePeerMemory(rank)
+        px = PeerExchange(None, words=1 + 67 * 3, group=None, memory=mem)
+        tables = (px.bufs_odd, px.bufs_even, px.flags, px.counter, px.rank, px.world)
+        px.close()
+        q.put((rank, tables, mem.log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_host_tables():
+    """dist.PeerExchange (the transport='peer' setup) over gloo with world
+    size 3: every rank assembles the same per-rank pointer tables (its own
+    allocations in its own slot, the others' opened from their handles),
+    sized buffers, and on close unmaps what it opened and frees what it
+    allocated."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_table_rank, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    want_odd = [1000 * (r + 1) + 1 for r in range(world)]
+    want_even = [1000 * (r + 1) + 2 for r in range(world)]
+    want_flags = [1000 * (r + 1) + 3 for r in range(world)]
+    for rank, (odd, even, flags, counter, rk, w), log in res:
+        assert rk == rank and w == world
+        assert odd == want_odd and even == want_even and flags == want_flags
+        assert counter == 1000 * (rank + 1) + 4
+        allocs = [e for e in log if e[0] == "alloc"]
+        assert [a[2] for a in allocs] == [8 * (1 + 67 * 3), 8 * (1 + 67 * 3), 8 * world, 4]
+        opened = sorted(e[1] for e in log if e[0] == "open")
+        closed = sorted(e[1] for e in log if e[0] == "close")
+        assert opened == closed and len(opened) == 3 * (world - 1)
+        assert all(p // 1000 != rank + 1 for p in opened)
+        assert sorted(e[1] for e in log if e[0] == "free") == sorted(a[1] for a in allocs)
