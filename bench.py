@@ -203,6 +203,20 @@ def run_ours(args, rank, world, local_rank):
     n0, n1 = rank * m // world, (rank + 1) * m // world
     xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
     run.set_exchange(xbuf.data_ptr())
+    # --transport peer (N > 1): K1 writes every rank's exchange buffer over
+    # peer memory and no collective runs in the step (one PeerExchange per run)
+    peer = dist is not None and args.transport == "peer"
+    exchanges = []
+
+    def attach_peers(r):
+        if peer:
+            from paper_2202_01753_b200.dist import PeerExchange
+            torch.cuda.synchronize()
+            px = PeerExchange(ctx, r.exchange_words())
+            px.attach(r)
+            exchanges.append(px)
+
+    attach_peers(run)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(it, k1_events=None):
@@ -212,7 +226,7 @@ def run_ours(args, rank, world, local_rank):
         if k1_events:
             k1_events[1].record(stream)
         run.reduce(it)
-        if dist is not None:
+        if dist is not None and not peer:
             dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
         run.finish(it)
 
@@ -265,13 +279,14 @@ def run_ours(args, rank, world, local_rank):
                        tau_rel=1e-15, seed=1, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=args.rng)
     run2 = M.Run(f, cfg2, ctx)
     run2.set_exchange(xbuf.data_ptr())
+    attach_peers(run2)
     out_edges = np.zeros(DIMS * N_BINS)
 
     def e2e_step(it):
         run2.set_grid(host_edges)                # H2D: the step's input grid
         run2.sample(it, n0, n1)
         run2.reduce(it)
-        if dist is not None:
+        if dist is not None and not peer:
             dist.all_reduce(xbuf)
         run2.finish(it)
         run2.grid_into(out_edges)                # D2H: adapted grid (synchronises)
@@ -313,7 +328,10 @@ def run_ours(args, rank, world, local_rank):
         "data": DATA[args.rng],
         "config": {"workload": "8D Genz f4 adjusting m-Cubes iteration", "integrand": "f4", "dims": DIMS,
                    "n_bins": N_BINS, "maxcalls": args.maxcalls, "m": m, "p": p, "evals_per_step": evals_per_step,
-                   "parallelism": f"cube-range partition x{world} + exact all-reduce" if world > 1 else "single GPU",
+                   "parallelism": (f"cube-range partition x{world} + " +
+                                   ("exact exchange over peer memory inside K1" if peer
+                                    else f"exact all-reduce ({dist.get_backend()})"))
+                                  if world > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) between timed steps", "rng": RNG_DESC[args.rng],
                    "reductions": REDUCTIONS[args.rng]},
         "clocks": clk,
@@ -340,13 +358,14 @@ def run_ours(args, rank, world, local_rank):
                            tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng="compat")
         run3 = M.Run(f, cfg3, ctx)
         run3.set_exchange(xbuf.data_ptr())
+        attach_peers(run3)
 
         def step3(it, evs):
             evs[0].record(stream)
             run3.sample(it, n0, n1)
             evs[1].record(stream)
             run3.reduce(it)
-            if dist is not None:
+            if dist is not None and not peer:
                 dist.all_reduce(xbuf)
             run3.finish(it)
 
@@ -382,13 +401,16 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu_baseline()
         line["time_to_epsrel"] = time_to_epsrel(M, ctx)
     elif world > 1 and not args.no_cpu:
-        tte = time_to_epsrel_dist(M, ctx, dist, dev, rank)
+        tte = time_to_epsrel_dist(M, ctx, dist, dev, rank, "peer" if peer else "collective")
         if rank == 0:
             line["time_to_epsrel"] = tte
     if rank == 0:
         print(json.dumps(line), flush=True)
     run.close()
     run2.close()
+    torch.cuda.synchronize()
+    for px in exchanges:  # collective: every rank unmaps, then frees
+        px.close()
     return 0
 
 
@@ -457,7 +479,7 @@ def time_to_epsrel(M, ctx):
     return out
 
 
-def time_to_epsrel_dist(M, ctx, dist, dev, rank):
+def time_to_epsrel_dist(M, ctx, dist, dev, rank, transport="collective"):
     """time_to_epsrel at N GPUs: paper_2202_01753_b200.dist.integrate (cube
     ranges per rank, exact all-reduce per iteration), wall time max over ranks;
     the reference CPU integrate is timed on rank 0's host cores."""
@@ -470,11 +492,11 @@ def time_to_epsrel_dist(M, ctx, dist, dev, rank):
     cfg = M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=1, lower=[0.0] * d,
                       upper=[1.0] * d)
     f = M.make_suite_integrand(5, d)
-    mdist.integrate(f, cfg, ctx=ctx)  # warm
+    mdist.integrate(f, cfg, ctx=ctx, transport=transport)  # warm
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    r = mdist.integrate(f, cfg, ctx=ctx)
+    r = mdist.integrate(f, cfg, ctx=ctx, transport=transport)
     ms = 1e3 * (time.perf_counter() - t0)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -599,6 +621,9 @@ def main():
     ap.add_argument("--rng", choices=["philox", "compat"], default="philox",
                     help="philox = the north-star stream (headline); compat = the reference's stream, bit-exact")
     ap.add_argument("--no-compat", action="store_true", help="skip the secondary compat-stream measurement")
+    ap.add_argument("--transport", choices=["collective", "peer"], default="collective",
+                    help="N > 1: exchange through an NCCL all-reduce, or K1 writing every rank's buffer over "
+                         "peer memory (CUDA IPC over NVLink)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
     ap.add_argument("--suite", default=None, help="run BASELINE configs 1-5 (GPU + reference CPU) into this JSONL")
     args = ap.parse_args()
