@@ -313,13 +313,25 @@ def run_ours(args, rank, world, local_rank):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
     peak_tflops = sms * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
-    traffic = None
+    # DRAM bytes and thread instructions per eval of this stream's K1, from the
+    # committed ncu capture (tools/summarize_ncu.py -> profiles/k1_traffic.json)
+    traffic, winst_per_eval, ncu_src = None, None, None
     tf_path = os.path.join(HERE, "profiles", "k1_traffic.json")
     if os.path.exists(tf_path):
         try:
-            traffic = json.load(open(tf_path)).get("bytes_per_launch")
+            ent = json.load(open(tf_path)).get(args.rng) or {}
+            traffic, winst_per_eval, ncu_src = (ent.get("bytes_per_launch"), ent.get("warp_instr_per_eval"),
+                                                ent.get("source"))
         except (OSError, ValueError):
-            traffic = None
+            pass
+    issue = None
+    if winst_per_eval:
+        # the instruction-issue roofline: 4 warp schedulers per SM, one issue each per clock;
+        # warp instructions per eval from the ncu capture (smsp__inst_executed.sum / evals)
+        ach = k1_evals * winst_per_eval / k1_avg_s / 1e9
+        pk = sms * 4 * sm_max * 1e6 / 1e9
+        issue = {"achieved": ach, "peak": pk, "unit": "G warp-instructions/s", "frac": ach / pk,
+                 "warp_instr_per_eval": winst_per_eval, "source": ncu_src}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -340,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 8 * DIMS * N_BINS,
                 "path": "C ABI mcb_run_set_grid/sample/reduce/finish/grid (host grid in, host grid out)"},
         "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
-                     "frac": achieved_tflops / peak_tflops, "traffic": traffic,
+                     "frac": achieved_tflops / peak_tflops, "traffic": traffic, "issue": issue,
                      "kernel": f"vsample_kernel<F4,8,{args.rng}>", "kernel_ms": 1e3 * k1_avg_s,
                      "ops_per_eval": OPS_PER_EVAL,
                      "peak_source": f"FP64 issue: {sms} SMs x {FP64_LANES_PER_SM} lanes x {sm_max:.0f} MHz "

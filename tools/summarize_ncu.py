@@ -98,8 +98,21 @@ def main():
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get("dram__bytes_read.sum", "byte"), 1)
     with open(os.path.join(ROOT, "profiles", f"ncu_k1_{tag}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    with open(os.path.join(ROOT, "profiles", "k1_traffic.json"), "w") as fh:
-        json.dump({"bytes_per_launch": dram * scale, "source": f"profiles/ncu_k1_{tag}.md", "kernel": name}, fh)
+    # per-stream entry (vsample_kernel<F, D, Rng, NB>: Rng 1 = philox, 0 = compat), read by bench.py
+    tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        table = json.load(open(tf))
+        if "bytes_per_launch" in table:  # the older flat format
+            table = {}
+    except (OSError, ValueError):
+        table = {}
+    targs = [a.strip() for a in name.split("<", 1)[1].split(">", 1)[0].split(",")] if "<" in name else []
+    rng = "philox" if len(targs) > 2 and targs[2] == "1" else "compat"
+    winst = float(m.get("smsp__inst_executed.sum", 0) or 0)
+    table[rng] = {"bytes_per_launch": dram * scale, "source": f"profiles/ncu_k1_{tag}.md", "kernel": name,
+                  "warp_instr_per_eval": (winst / evals) if (evals and winst) else None}
+    with open(tf, "w") as fh:
+        json.dump(table, fh, indent=1)
 
     # launch list
     rows = list(csv.reader(open(launches)))
