@@ -50,6 +50,16 @@ inline bool pdl_enabled() {
   return on;
 }
 
+/// MCB_FULL_BLOCKS=1: K1 always launches full blocks (A/B timing of the
+/// small-problem block sizing; same bits either way).
+inline bool full_blocks_forced() {
+  static const bool on = [] {
+    const char* v = std::getenv("MCB_FULL_BLOCKS");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 /// Block-wide grid adaptation in the finish kernel (adjust_grid_par);
 /// MCB_ADJ_PAR=0 selects the warp-per-axis form (same bits, for A/B timing).
 inline bool adjust_par_enabled() {
@@ -290,7 +300,6 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
                  unsigned long long* err_key, unsigned long long* words) {
   auto kern = vsample_kernel<F, D, R, NB>;
   constexpr int kThreads = sample_threads(R, D);
-  constexpr int kWalkers = kThreads;  // threads that walk cubes
   Launch L;
   L.pnb = partial_bins(R, sh.nb);
   L.smem = sample_smem_bytes(D, L.pnb, bin_axes);
@@ -309,8 +318,22 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   }
   const int occ = std::max(cached_occ, 1);
   const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
-  const std::uint64_t want = (work + kWalkers - 1) / kWalkers;
+  const std::uint64_t want = (work + kThreads - 1) / kThreads;
   L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
+  // Threads per block: the fewest (whole warps) that keep the per-thread cube
+  // count of a full block.  Small problems then run every thread over the
+  // same number of cubes instead of a last wave of partly idle warps (C1:
+  // 2.45 cubes per thread at 1024 -> 3 each at 864 threads).  Row mode
+  // (large problems) keeps full blocks.
+  int threads = kThreads;
+  if (!row_mode(sh) && work > 0 && !full_blocks_forced()) {
+    const std::uint64_t full = static_cast<std::uint64_t>(L.blocks) * kThreads;
+    const std::uint64_t per = (work + full - 1) / full;
+    const std::uint64_t need = (work + static_cast<std::uint64_t>(L.blocks) * per - 1) /
+                               (static_cast<std::uint64_t>(L.blocks) * per);
+    threads = static_cast<int>(std::min<std::uint64_t>(kThreads, (need + 31) / 32 * 32));
+  }
+  const int walkers = threads;  // threads that walk cubes
 
   SampleArgs a{};
   a.edges = ctx.edges.get();
@@ -333,7 +356,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.n0 = n0;
   a.n1 = n1;
   a.A = sh.A;
-  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * kWalkers;
+  const std::uint64_t T = static_cast<std::uint64_t>(L.blocks) * walkers;
   // Row mode when there are >= 2^20 rows (of g cubes along axis 0).  The
   // n -> cube map must depend on the problem only (m, g, d), never on the
   // slice [n0, n1) or the launch, so that slices sampled by different ranks
@@ -369,7 +392,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.err_key = err_key;
   a.stop = stop;
   a.peer = ctx.peer;
-  launch_pdl(kern, L.blocks, kThreads, L.smem, ctx.stream(), a, f);
+  launch_pdl(kern, L.blocks, threads, L.smem, ctx.stream(), a, f);
   ++ctx.launches;
   return L;
 }
