@@ -50,6 +50,15 @@ inline bool pdl_enabled() {
   return on;
 }
 
+/// MCB_K1_CLUSTER=0: K1 without 2-CTA clusters (each CTA flushes its own words).
+inline bool k1_cluster_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MCB_K1_CLUSTER");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 /// MCB_FULL_BLOCKS=1: K1 always launches full blocks (A/B timing of the
 /// small-problem block sizing; same bits either way).
 inline bool full_blocks_forced() {
@@ -73,21 +82,37 @@ inline bool adjust_par_enabled() {
 /// kern<<<grid, block, smem, stream>>>(args...) with programmatic stream
 /// serialisation (the kernel must pdl_wait() before reading its
 /// predecessor's output).
+/// launch_pdl with thread-block clusters of `cluster` CTAs along x (1: none).
 template <class... KArgs, class... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
-                Args&&... args) {
+void launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
+                        unsigned cluster, Args&&... args) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
   lc.blockDim = block;
   lc.dynamicSmemBytes = smem;
   lc.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   lc.attrs = at;
   lc.numAttrs = 1;
+  if (cluster > 1) {
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cluster;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    lc.numAttrs = 2;
+  }
   MCB_CUDA(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
 }
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
+                Args&&... args) {
+  launch_pdl_cluster(kern, grid, block, smem, stream, 1, std::forward<Args>(args)...);
+}
+
+
 
 template <class T>
 class DevBuf {
@@ -392,7 +417,12 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   a.err_key = err_key;
   a.stop = stop;
   a.peer = ctx.peer;
-  launch_pdl(kern, L.blocks, threads, L.smem, ctx.stream(), a, f);
+  // pairs of CTAs in a cluster split the flush (each adds both CTAs' words
+  // for half of the accumulators, read over DSMEM): half the global
+  // reductions per SM.  Two-CTA clusters keep all 148 SMs usable at one CTA
+  // per SM (tools/microbench/clusters.cu).
+  const unsigned cluster = (L.blocks % 2 == 0 && k1_cluster_enabled()) ? 2u : 1u;
+  launch_pdl_cluster(kern, L.blocks, threads, L.smem, ctx.stream(), cluster, a, f);
   ++ctx.launches;
   return L;
 }

@@ -29,6 +29,8 @@
 //    exchange buffer (exact 64-bit integer atomics; see the flush below).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdint>
 #include <span>
@@ -521,25 +523,49 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     }
   };
   {
+    // In a 2-CTA cluster each CTA adds BOTH CTAs' words (its own + its
+    // partner's over DSMEM; the u64 sums of two u32 words are exact) for one
+    // half of the words: half the global reductions per SM.
+    namespace cg = cooperative_groups;
+    const cg::cluster_group cluster = cg::this_cluster();
+    const unsigned csize = cluster.num_blocks();
+    const unsigned crank = cluster.block_rank();
+    const std::uint32_t* peer_acc = acc;
+    if (csize == 2) {
+      cluster.sync();  // the partner's accumulators are final
+      peer_acc = cluster.map_shared_rank(acc, crank ^ 1u);
+    }
+    const std::uint32_t* peer_bins = peer_acc + kScalarAccs * kLaneCopies * kXWords;
     const int ncells = static_cast<int>(a.bin_axes * nb);
-    for (int i = tid; i < ncells * kXWords; i += nt) {
-      const std::uint32_t v = bins[i];
+    const int nbw = ncells * kXWords;
+    const int b0 = csize == 2 ? (crank ? nbw / 2 : 0) : 0, b1 = csize == 2 ? (crank ? nbw : nbw / 2) : nbw;
+    for (int i = b0 + tid; i < b1; i += nt) {
+      const unsigned long long v = static_cast<unsigned long long>(bins[i]) +
+                                   (csize == 2 ? static_cast<unsigned long long>(peer_bins[i]) : 0ull);
       if (!v) continue;
       const int c = i / kXWords, w = i - c * kXWords;
       const int ax = c / static_cast<int>(nb), cell = c - ax * static_cast<int>(nb);
       const int slot = ax * static_cast<int>(a.nb_out) + min(cell, static_cast<int>(a.nb_out) - 1);
-      add_word(static_cast<std::ptrdiff_t>(kScalarAccs + slot) * kXWords + w, static_cast<unsigned long long>(v));
+      add_word(static_cast<std::ptrdiff_t>(kScalarAccs + slot) * kXWords + w, v);
     }
-    // est+/est-/var: the 32 lane copies folded into u64 word sums (< 2^37, exact)
-    for (int i = tid; i < kScalarAccs * kXWords; i += nt) {
+    // est+/est-/var: the 32 lane copies (of both CTAs) folded into u64 word sums (< 2^38, exact)
+    const int nsw = kScalarAccs * kXWords;
+    const int s0 = csize == 2 ? (crank ? nsw / 2 : 0) : 0, s1 = csize == 2 ? (crank ? nsw : nsw / 2) : nsw;
+    for (int i = s0 + tid; i < s1; i += nt) {
       const int kind = i / kXWords, w = i % kXWords;
       const std::uint32_t* src = acc + kind * kLaneCopies * kXWords + w;
+      const std::uint32_t* psrc = peer_acc + kind * kLaneCopies * kXWords + w;
       unsigned long long sum = 0;
 #pragma unroll 8
       for (int l = 0; l < kLaneCopies; ++l) sum += src[l * kXWords];
+      if (csize == 2) {
+#pragma unroll 8
+        for (int l = 0; l < kLaneCopies; ++l) sum += psrc[l * kXWords];
+      }
       if (sum) add_word(i, sum);
     }
-    if (tid == 0 && nonfinite_s) add_word(-1, nonfinite_s);  // words[-1]: the non-finite count
+    if (tid == 0 && nonfinite_s) add_word(-1, nonfinite_s);  // words[-1]: the non-finite count (own CTA's)
+    if (csize == 2) cluster.sync();  // the partner has finished reading this CTA's accumulators
   }
   if (npeers) {
     // Publish "this rank's words are in": every thread's reductions are

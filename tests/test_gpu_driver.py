@@ -236,8 +236,9 @@ print("|".join(out))
 
 def test_launch_switches_give_the_same_bits():
     """Programmatic dependent launch (MCB_PDL), the block-wide grid
-    adaptation (MCB_ADJ_PAR) and K1's small-problem block sizing
-    (MCB_FULL_BLOCKS) change only how the kernels are scheduled: every
+    adaptation (MCB_ADJ_PAR), K1's small-problem block sizing
+    (MCB_FULL_BLOCKS) and its 2-CTA cluster flush (MCB_K1_CLUSTER) change
+    only how the kernels are scheduled: every
     combination yields the same estimates, sigmas and per-iteration grids
     (observer path and lookahead path alike)."""
     import os
@@ -247,12 +248,14 @@ def test_launch_switches_give_the_same_bits():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     code = _SWITCH_CASE.format(root=root)
     res = {}
-    for pdl, par, full in (("1", "1", "0"), ("0", "1", "0"), ("1", "0", "0"), ("0", "0", "0"), ("1", "1", "1")):
-        env = dict(os.environ, MCB_PDL=pdl, MCB_ADJ_PAR=par, MCB_FULL_BLOCKS=full)
+    for pdl, par, full, clu in (("1", "1", "0", "1"), ("0", "1", "0", "1"), ("1", "0", "0", "1"),
+                                ("0", "0", "0", "1"), ("1", "1", "1", "1"), ("1", "1", "0", "0"),
+                                ("0", "0", "1", "0")):
+        env = dict(os.environ, MCB_PDL=pdl, MCB_ADJ_PAR=par, MCB_FULL_BLOCKS=full, MCB_K1_CLUSTER=clu)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
-        res[(pdl, par, full)] = p.stdout.strip().splitlines()[-1]
-    first = res[("1", "1", "0")]
+        res[(pdl, par, full, clu)] = p.stdout.strip().splitlines()[-1]
+    first = res[("1", "1", "0", "1")]
     for row in first.split("|"):
         e1, e2, _, _ = row.split()
         assert e1 == e2  # observer and lookahead loops agree
