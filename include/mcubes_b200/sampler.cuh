@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   const int npeers = a.peer.npeers;
   auto add_word = [&](std::ptrdiff_t idx, unsigned long long v) {
     if (npeers == 0) {
-      atomicAdd(a.words + idx, v);
+      red_add_gpu(a.words + idx, v);
     } else {
       for (int q = 0; q < npeers; ++q) red_add_sys(a.peer.words[q] + idx, v);
     }
