@@ -3,21 +3,24 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+One "step" = one full adjusting m-Cubes iteration -- V-Sample (K1, with its
+exact cross-block sum into the exchange words), [the all-reduce across
+ranks], rounding, grid adaptation, weighted estimate and convergence gate --
+of 8D Genz f4 (Gaussian) at maxcalls = 1e9: m = 12^8 = 429,981,696 sub-cubes,
+p = 2, so 8.6e8 integrand evaluations per step (BASELINE config 2's largest
+8D shape).  The grid starts uniform and adapts every step (warm-up steps
+included), on both arms.  value = evals/s over the whole job, device-timed
+with CUDA events, max over ranks; L2 is flushed (256 MiB write) between timed
+steps.  Secondary GPU-only line: the same step at maxcalls 1e10 (m = 2^32).
+
 Under torchrun (N > 1) there is one process per GPU; rank r samples its slice
-of the linear work index and the exact per-iteration exchange buffer
-(est/var/contribution superaccumulator words, include/mcubes_b200.h
-MCB_XWORDS) is all-reduced over NCCL before every rank finishes the
-iteration identically (grid adaptation + weighted estimate on device).
+of the linear work index and the exact exchange buffer is all-reduced over
+NCCL before every rank finishes the iteration identically.
 
-One "step" = one full adjusting m-Cubes iteration (V-Sample K1, exact
-cross-block reduction K3a, [all-reduce], rounding K3b, grid adaptation +
-weighted estimate + convergence gate K4) of 8D Genz f4 (Gaussian) at
-maxcalls = 1e10 (m = 16^8 = 2^32 sub-cubes, p = 2: 8.59e9 integrand evals per
-step).  value = evals/s over the whole job, device-timed with CUDA events, max
-over ranks; L2 is flushed (256 MiB write) between timed steps.
-
---impl reference runs the reference CPU library (oracle/_ref/libmcubes_ref.so,
-compiled from /root/reference's own headers) on the host cores, rank 0 only.
+--impl reference runs the SAME workload through the reference CPU library
+(oracle/_ref/libmcubes_ref.so: the unmodified /root/reference headers
+compiled in place): v_sample + Grid::adjusted + weighted_estimate per step
+(driver.hpp:231-252) on the evolving grid, all host threads, rank 0 only.
 """
 from __future__ import annotations
 
@@ -38,27 +41,41 @@ METRIC = "integrand evals/sec (m-Cubes adjusting iteration, 8D Genz f4)"
 UNIT = "evals/s"
 DIMS = 8
 FAMILY = 4
-MAXCALLS = 10 ** 10
+MAXCALLS = 10 ** 9
+MAXCALLS_LARGE = 10 ** 10  # secondary GPU-only line: m = 16^8 = 2^32 cubes
 N_BINS = 50
+ALPHA = 1.5
 # Algorithmic FP64 ops per eval (SURVEY.md 8d convention: +-*/ = 1, exp = 20):
 # map 10d + accumulate (9 + 1 + bin_axes) + integrand f4 (3d + 21).
 OPS_PER_EVAL = 10 * DIMS + (9 + 1 + DIMS) + (3 * DIMS + 21)  # = 143 for d = 8
 FP64_LANES_PER_SM = 64
-REF_SAMPLE_MAXCALLS = 10 ** 8  # bounded CPU sample (m = 9^8, p = 2: 86.1M evals)
 RNG_DESC = {
     "philox": "philox (north-star Philox4x32-10 keyed by (seed, iteration), counter (cube, sample, axis block); "
               "FMA transform; statistically equivalent to the reference, bitwise equal to its C twin)",
     "compat": "compat (the reference's keyed SplitMix stream and arithmetic order; bitwise equal to the reference)",
+    "reference": "the reference's keyed SplitMix stream (rng.hpp), its own code",
 }
-REDUCTIONS = {
-    "philox": "estimate/variance exact (superaccumulator); bins: (f J)^2 rounded to 24 significant bits, "
-              "summed exactly (deterministic, geometry- and GPU-count-independent)",
-    "compat": "exact (superaccumulator), as the reference's ExactSum/ExactBins",
+BINS_DESC = {
+    "r24": "estimate/variance exact (superaccumulator); bins: (f J)^2 rounded to 24 significant bits, then "
+           "summed exactly (deterministic, geometry- and GPU-count-independent)",
+    "exact": "exact (superaccumulator): estimate, variance and bins, as the reference's ExactSum/ExactBins",
 }
 DATA = {
     "philox": "synthetic (counter-based Philox stream; no input data)",
     "compat": "synthetic (keyed SplitMix stream of the reference; no input data)",
+    "reference": "synthetic (keyed SplitMix stream of the reference; no input data)",
 }
+
+
+def workload(maxcalls: int, m: int, p: int) -> dict:
+    """The `config` both arms report -- the workload only (implementation
+    details go to top-level keys), so the two lines describe the same job."""
+    return {"workload": "8D Genz f4 (Gaussian): one adjusting m-Cubes iteration per step (V-Sample, exact "
+                        "reductions, grid adaptation, weighted estimate); grid uniform at step 1, adapted every step",
+            "integrand": "f4", "dims": DIMS, "n_bins": N_BINS, "alpha": ALPHA, "maxcalls": maxcalls, "m": m, "p": p,
+            "evals_per_step": m * p, "seed": 0,
+            "l2": "GPU arm: flushed (256 MiB write) between timed steps; CPU arm: per-step working set "
+                  "(m * p evaluations) far beyond the host caches"}
 
 
 def log(*a):
@@ -124,26 +141,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def ref_v_sample_rate(maxcalls: int, steps: int, warmup: int, threads: int, seed0: int = 0):
-    """Time the reference's own v_sample (oracle/_ref) on `threads` host cores."""
-    import numpy as np  # noqa: F401
+def ref_adjusting_steps(maxcalls: int, steps: int, warmup: int, threads: int, seed: int = 0):
+    """The reference's own adjusting iteration, timed per step on `threads`
+    host cores: v_sample, Grid::adjusted and weighted_estimate
+    (driver.hpp:231-252) through oracle/_ref, on the evolving grid (uniform at
+    step 1).  Returns (per-step seconds of the timed steps, m, p, result)."""
     import oracle as O
 
     lower, upper = [0.0] * DIMS, [1.0] * DIMS
     sp = (O._U64 * 4)()
     lib = O.ref()
-    rc = lib.ref_setup(DIMS, N_BINS, maxcalls, 15, 10, 1e-3, 1.5, 1.5, O.darr(lower), O.darr(upper), threads, sp)
+    rc = lib.ref_setup(DIMS, N_BINS, maxcalls, 15, 10, 1e-3, ALPHA, 1.5, O.darr(lower), O.darr(upper), threads, sp)
     assert rc == 0, lib.ref_last_error()
-    m, p = sp[1], sp[2]
-    times = []
-    for it in range(warmup + steps):
+    m, s, p = sp[1], sp[3], sp[2]
+    edges = O.uniform_edges(DIMS, N_BINS, lower, upper)
+    he, hv, times = [], [], []
+    est = (0.0, 0.0, 0.0)
+    for it in range(1, warmup + steps + 1):
         t0 = time.perf_counter()
-        O.v_sample("ref", FAMILY, None, DIMS, N_BINS, lower, upper, None, m, sp[3], p, seed0, it + 1, "all", threads)
+        r = O.v_sample("ref", FAMILY, None, DIMS, N_BINS, lower, upper, edges, m, s, p, seed, it, "all", threads)
+        edges = O.grid_adjust("ref", DIMS, N_BINS, lower, upper, edges, r["contrib"], ALPHA)
+        he.append(r["est"])
+        hv.append(r["var"])
+        est = O.weighted_estimate(he, hv)
         dt = time.perf_counter() - t0
-        if it >= warmup:
+        if it > warmup:
             times.append(dt)
-    total = sum(times)
-    return m * p * len(times) / total, m, p, total
+    return times, m, p, {"estimate": est[0], "sigma": est[1], "chi2_dof": est[2]}
 
 
 def run_reference(args, rank):
@@ -155,18 +179,22 @@ def run_reference(args, rank):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmcubes_ref.so not built"}))
         return 0
     threads = os.cpu_count() or 1
-    rate, m, p, total = ref_v_sample_rate(REF_SAMPLE_MAXCALLS, args.steps, args.warmup, threads)
-    sample = (f"reference v_sample (oracle/_ref, compiled from /root/reference headers) on 8D f4 at "
-              f"maxcalls=1e8 (m={m}, p={p}: {m * p} evals/step), {threads} threads")
+    times, m, p, res = ref_adjusting_steps(args.maxcalls, args.steps, args.warmup, threads)
+    total = sum(times)
+    rate = m * p * len(times) / total
+    sample = (f"the full workload every step: reference v_sample + Grid::adjusted + weighted_estimate "
+              f"(oracle/_ref, compiled from /root/reference headers) at maxcalls={args.maxcalls:.0e} "
+              f"(m={m}, p={p}: {m * p} evals/step), {threads} threads, {args.warmup} untimed + "
+              f"{args.steps} timed steps, {total:.1f} s timed")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (keyed RNG stream, no inputs)",
-        "config": {"workload": "8D Genz f4 adjusting iteration", "dims": DIMS, "n_bins": N_BINS,
-                   "maxcalls": REF_SAMPLE_MAXCALLS, "m": m, "p": p, "integrand": "f4"},
+        "data": DATA["reference"], "config": workload(args.maxcalls, m, p),
+        "rng": RNG_DESC["reference"], "bins": "exact", "parallelism": f"{threads} host threads",
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result": res,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -194,102 +222,109 @@ def run_ours(args, rank, world, local_rank):
     ctx = M.Context(gpu)
     ctx.set_stream(stream.cuda_stream)
     f = M.make_suite_integrand(FAMILY, DIMS)
-    total_its = args.warmup + args.steps
-    cfg = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
-                      tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=args.rng)
-    run = M.Run(f, cfg, ctx)
-    sp = M.setup(cfg)
-    m, p = sp.m, sp.p
-    n0, n1 = rank * m // world, (rank + 1) * m // world
-    xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
-    run.set_exchange(xbuf.data_ptr())
     # --transport peer (N > 1): K1 writes every rank's exchange buffer over
     # peer memory and no collective runs in the step (one PeerExchange per run)
     peer = dist is not None and args.transport == "peer"
     exchanges = []
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def attach_peers(r):
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def make_run(maxcalls, rng, bins, its, seed):
+        cfg = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=maxcalls, itmax=its, ita=its, tau_rel=1e-15,
+                          alpha=ALPHA, seed=seed, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=rng, bins=bins)
+        run = M.Run(f, cfg, ctx)
+        xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
+        run.set_exchange(xbuf.data_ptr())
         if peer:
             from paper_2202_01753_b200.dist import PeerExchange
             torch.cuda.synchronize()
-            px = PeerExchange(ctx, r.exchange_words())
-            px.attach(r)
+            px = PeerExchange(ctx, run.exchange_words())
+            px.attach(run)
             exchanges.append(px)
+        m = run.work_items
+        return run, xbuf, m, rank * m // world, (rank + 1) * m // world
 
-    attach_peers(run)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    def measure(maxcalls, rng, bins, steps, warmup, seed=0, clocks=None):
+        """W warm-up + K timed adjusting steps of one run: the grid starts
+        uniform and adapts every step.  Device-timed with CUDA events (whole
+        step, and K1 alone for the roofline), max over ranks."""
+        run, xbuf, m, n0, n1 = make_run(maxcalls, rng, bins, warmup + steps, seed)
 
-    def step(it, k1_events=None):
-        if k1_events:
-            k1_events[0].record(stream)
-        run.sample(it, n0, n1)
-        if k1_events:
-            k1_events[1].record(stream)
-        run.reduce(it)
-        if dist is not None and not peer:
-            dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
-        run.finish(it)
+        def step(it, k1_events=None):
+            if k1_events:
+                k1_events[0].record(stream)
+            run.sample(it, n0, n1)
+            if k1_events:
+                k1_events[1].record(stream)
+            run.reduce(it)
+            if dist is not None and not peer:
+                dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
+            run.finish(it)
 
-    # warm-up (also compiles/loads everything)
-    for it in range(1, args.warmup + 1):
-        step(it)
-        flush.zero_()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
+        for it in range(1, warmup + 1):
+            step(it)
+            flush.zero_()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        launches0 = ctx.launches
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        k1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        for i in range(steps):
+            ev[i][0].record(stream)
+            step(warmup + 1 + i, k1[i])
+            ev[i][1].record(stream)
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        launches = ctx.launches - launches0
+        clk = clocks.stop() if clocks else None
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        k1_ms = [a.elapsed_time(b) for a, b in k1]
+        total_ms = max_over_ranks(sum(step_ms))
+        res = run.result()
+        assert res.iterations_used == warmup + steps and np.isfinite(res.estimate), res
+        run.close()
+        p = res.params.p
+        k1_s = 1e-3 * statistics.mean(k1_ms)
+        return {"value": m * p * steps / (total_ms * 1e-3), "ms_per_step": total_ms / steps, "m": m, "p": p,
+                "k1_s": k1_s, "k1_evals": (n1 - n0) * p, "share": 1e3 * k1_s * steps / sum(step_ms),
+                "launches": launches, "clocks": clk, "result": res}
 
+    # ---- the headline: device-timed steps with inputs resident in HBM
     clocks = ClockSampler(gpu) if rank == 0 else None
-    if clocks:
-        clocks.start()
-        time.sleep(0.3)
-    launches0 = ctx.launches
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    k1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    for i in range(args.steps):
-        it = args.warmup + 1 + i
-        ev[i][0].record(stream)
-        step(it, k1[i])
-        ev[i][1].record(stream)
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    launches = ctx.launches - launches0
-    clk = clocks.stop() if clocks else None
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    k1_ms = [a.elapsed_time(b) for a, b in k1]
-    total_ms = sum(step_ms)
-    if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    res = run.result()
-    assert res.iterations_used == total_its and np.isfinite(res.estimate), res
+    head = measure(args.maxcalls, args.rng, args.bins, args.steps, args.warmup, clocks=clocks)
+    m, p = head["m"], head["p"]
+    res = head["result"]
 
-    evals_per_step = m * p
-    value = evals_per_step * args.steps / (total_ms * 1e-3)
-
-    # ---- end to end through the C ABI with host buffers (H2D grid in, D2H result out)
+    # ---- end to end through the C ABI with host buffers (H2D grid in, D2H adapted grid out)
+    run2, xbuf2, _, n0, n1 = make_run(args.maxcalls, args.rng, args.bins, args.warmup + args.steps, 1)
     host_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
-    host_edges[:] = run.grid().raw_edges
-    cfg2 = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
-                       tau_rel=1e-15, seed=1, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng=args.rng)
-    run2 = M.Run(f, cfg2, ctx)
-    run2.set_exchange(xbuf.data_ptr())
-    attach_peers(run2)
-    out_edges = np.zeros(DIMS * N_BINS)
+    host_edges[:] = np.asarray(M.Grid(DIMS, N_BINS, [0.0] * DIMS, [1.0] * DIMS).raw_edges)
+    out_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
 
     def e2e_step(it):
         run2.set_grid(host_edges)                # H2D: the step's input grid
         run2.sample(it, n0, n1)
         run2.reduce(it)
         if dist is not None and not peer:
-            dist.all_reduce(xbuf)
+            dist.all_reduce(xbuf2)
         run2.finish(it)
         run2.grid_into(out_edges)                # D2H: adapted grid (synchronises)
+        host_edges[:] = out_edges                # the next step samples on it
 
     for it in range(1, args.warmup + 1):
         e2e_step(it)
@@ -298,28 +333,22 @@ def run_ours(args, rank, world, local_rank):
     t0 = time.perf_counter()
     for i in range(args.steps):
         e2e_step(args.warmup + 1 + i)
-    e2e_s = time.perf_counter() - t0
-    r2 = run2.result()  # D2H of estimate/variance history
-    if dist is not None:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = evals_per_step * args.steps / e2e_s
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    run2.result()
+    run2.close()
+    e2e_value = m * p * args.steps / e2e_s
 
     # ---- roofline of the dominant kernel (K1 vsample_kernel)
-    k1_avg_s = 1e-3 * statistics.mean(k1_ms)
-    k1_evals = (n1 - n0) * p
-    achieved_tflops = OPS_PER_EVAL * k1_evals / k1_avg_s / 1e12
+    achieved_tflops = OPS_PER_EVAL * head["k1_evals"] / head["k1_s"] / 1e12
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
+    sm_max = (head["clocks"] or {}).get("sm_max_mhz") or 1965.0
     peak_tflops = sms * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
-    # DRAM bytes and thread instructions per eval of this stream's K1, from the
-    # committed ncu capture (tools/summarize_ncu.py -> profiles/k1_traffic.json)
+    stream_key = args.rng if args.rng == "compat" else f"philox_{args.bins}"
     traffic, winst_per_eval, ncu_src = None, None, None
     tf_path = os.path.join(HERE, "profiles", "k1_traffic.json")
     if os.path.exists(tf_path):
         try:
-            ent = json.load(open(tf_path)).get(args.rng) or {}
+            ent = json.load(open(tf_path)).get(stream_key) or {}
             traffic, winst_per_eval, ncu_src = (ent.get("bytes_per_launch"), ent.get("warp_instr_per_eval"),
                                                 ent.get("source"))
         except (OSError, ValueError):
@@ -328,89 +357,62 @@ def run_ours(args, rank, world, local_rank):
     if winst_per_eval:
         # the instruction-issue roofline: 4 warp schedulers per SM, one issue each per clock;
         # warp instructions per eval from the ncu capture (smsp__inst_executed.sum / evals)
-        ach = k1_evals * winst_per_eval / k1_avg_s / 1e9
+        ach = head["k1_evals"] * winst_per_eval / head["k1_s"] / 1e9
         pk = sms * 4 * sm_max * 1e6 / 1e9
         issue = {"achieved": ach, "peak": pk, "unit": "G warp-instructions/s", "frac": ach / pk,
                  "warp_instr_per_eval": winst_per_eval, "source": ncu_src}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": DATA[args.rng],
-        "config": {"workload": "8D Genz f4 adjusting m-Cubes iteration", "integrand": "f4", "dims": DIMS,
-                   "n_bins": N_BINS, "maxcalls": args.maxcalls, "m": m, "p": p, "evals_per_step": evals_per_step,
-                   "parallelism": (f"cube-range partition x{world} + " +
-                                   ("exact exchange over peer memory inside K1" if peer
-                                    else f"exact all-reduce ({dist.get_backend()})"))
-                                  if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) between timed steps", "rng": RNG_DESC[args.rng],
-                   "reductions": REDUCTIONS[args.rng]},
-        "clocks": clk,
-        "gpu_launches": launches,
+        "config": workload(args.maxcalls, m, p),
+        "rng": RNG_DESC[args.rng], "bins": args.bins if args.rng == "philox" else "exact",
+        "reductions": BINS_DESC[args.bins if args.rng == "philox" else "exact"],
+        "parallelism": ((f"cube-range partition x{world} + " +
+                         ("exact exchange over peer memory inside K1" if peer
+                          else f"exact all-reduce ({dist.get_backend()})")) if world > 1 else "single GPU"),
+        "clocks": head["clocks"],
+        "gpu_launches": head["launches"],
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * DIMS * N_BINS,
                 "d2h_bytes_per_step": 8 * DIMS * N_BINS,
-                "path": "C ABI mcb_run_set_grid/sample/reduce/finish/grid (host grid in, host grid out)"},
+                "path": "C ABI mcb_run_set_grid/sample/reduce/finish/grid (host grid in, adapted host grid out, "
+                        "every step)"},
         "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved_tflops / peak_tflops, "traffic": traffic, "issue": issue,
-                     "kernel": f"vsample_kernel<F4,8,{args.rng}>", "kernel_ms": 1e3 * k1_avg_s,
+                     "kernel": f"vsample_kernel<F4,8,{stream_key}>", "kernel_ms": 1e3 * head["k1_s"],
                      "ops_per_eval": OPS_PER_EVAL,
                      "peak_source": f"FP64 issue: {sms} SMs x {FP64_LANES_PER_SM} lanes x {sm_max:.0f} MHz "
                                     "(MEASURED_PEAKS.json has no FP64 figure; profiles/microbench_r01.txt "
                                     "measures 1.75e13 DADD/s)",
-                     "share_of_step": 1e3 * k1_avg_s * args.steps / sum(step_ms)},
-        "result": {"estimate": res.estimate, "sigma": res.sigma, "chi2_dof": res.chi2_dof,
-                   "truth": f.reference},
+                     "share_of_step": head["share"]},
+        "result": {"estimate": res.estimate, "sigma": res.sigma, "chi2_dof": res.chi2_dof, "truth": f.reference,
+                   "samples": res.total_samples, "bin_writes": res.bin_writes},
     }
 
-    if args.rng == "philox" and not args.no_compat:
-        # the same step on the reference's own stream and arithmetic order
-        # (bitwise equal to the CPU reference): device-timed like `value`
-        cfg3 = M.RunConfig(dims=DIMS, n_bins=N_BINS, maxcalls=args.maxcalls, itmax=total_its, ita=total_its,
-                           tau_rel=1e-15, seed=0, lower=[0.0] * DIMS, upper=[1.0] * DIMS, rng="compat")
-        run3 = M.Run(f, cfg3, ctx)
-        run3.set_exchange(xbuf.data_ptr())
-        attach_peers(run3)
+    def secondary(maxcalls, rng, bins, steps, desc):
+        r = measure(maxcalls, rng, bins, steps, args.warmup)
+        ach = OPS_PER_EVAL * r["k1_evals"] / r["k1_s"] / 1e12
+        return {"value": r["value"], "unit": UNIT, "maxcalls": maxcalls, "m": r["m"], "p": r["p"], "rng": rng,
+                "bins": bins or "exact", "what": desc, "kernel_ms": 1e3 * r["k1_s"], "roofline_achieved": ach,
+                "roofline_frac": ach / peak_tflops,
+                "result": {"estimate": r["result"].estimate, "sigma": r["result"].sigma}}
 
-        def step3(it, evs):
-            evs[0].record(stream)
-            run3.sample(it, n0, n1)
-            evs[1].record(stream)
-            run3.reduce(it)
-            if dist is not None and not peer:
-                dist.all_reduce(xbuf)
-            run3.finish(it)
-
-        evs3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in range(args.warmup + args.steps)]
-        st3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        for it in range(1, args.warmup + 1):
-            step3(it, evs3[it - 1])
-            flush.zero_()
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        for i in range(args.steps):
-            st3[i][0].record(stream)
-            step3(args.warmup + 1 + i, evs3[args.warmup + i])
-            st3[i][1].record(stream)
-            flush.zero_()
-        torch.cuda.synchronize()
-        c_total = sum(a.elapsed_time(b) for a, b in st3)
-        if dist is not None:
-            t = torch.tensor([c_total], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            c_total = float(t.item())
-        c_k1 = 1e-3 * statistics.mean(a.elapsed_time(b) for a, b in evs3[args.warmup:])
-        c_ach = OPS_PER_EVAL * k1_evals / c_k1 / 1e12
-        line["compat"] = {"value": evals_per_step * args.steps / (c_total * 1e-3), "unit": UNIT,
-                          "rng": RNG_DESC["compat"], "kernel_ms": 1e3 * c_k1, "roofline_achieved": c_ach,
-                          "roofline_frac": c_ach / peak_tflops, "result": {"estimate": run3.result().estimate}}
-        run3.close()
+    if not args.no_secondary:
+        if args.rng == "philox" and args.bins == "r24":
+            line["philox_exact_bins"] = secondary(args.maxcalls, "philox", "exact", args.steps,
+                                                  "the same steps with exact bins (the reference's ExactBins "
+                                                  "precision)")
+        if args.rng == "philox":
+            line["compat"] = secondary(args.maxcalls, "compat", "", args.steps,
+                                       "the same steps on the reference's own stream and arithmetic order "
+                                       "(bitwise the reference)")
+        line["maxcalls_1e10"] = secondary(MAXCALLS_LARGE, args.rng, args.bins, min(args.steps, 5),
+                                          "GPU-only: 8D f4 at maxcalls 1e10 (m = 16^8 = 2^32 sub-cubes)")
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline"] = cpu_baseline(args.maxcalls)
         line["time_to_epsrel"] = time_to_epsrel(M, ctx)
     elif world > 1 and not args.no_cpu:
         tte = time_to_epsrel_dist(M, ctx, dist, dev, rank, "peer" if peer else "collective")
@@ -418,77 +420,110 @@ def run_ours(args, rank, world, local_rank):
             line["time_to_epsrel"] = tte
     if rank == 0:
         print(json.dumps(line), flush=True)
-    run.close()
-    run2.close()
     torch.cuda.synchronize()
     for px in exchanges:  # collective: every rank unmaps, then frees
         px.close()
     return 0
 
 
-def cpu_baseline():
+def cpu_baseline(maxcalls):
+    """The reference's own adjusting iteration at the bench workload, timed on
+    all host cores: one untimed step, then two timed (~10-20 s of CPU work)."""
     import oracle as O
 
     if not O.ref_available():
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
     threads = os.cpu_count() or 1
-    rate, m, p, total = ref_v_sample_rate(REF_SAMPLE_MAXCALLS, 2, 1, threads, seed0=7)
-    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"2 timed reference v_sample iterations of 8D f4 at maxcalls=1e8 (m={m}, p={p}), "
+    times, m, p, _ = ref_adjusting_steps(maxcalls, 2, 1, threads, seed=7)
+    total = sum(times)
+    return {"value": m * p * len(times) / total, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"the same workload: 2 timed reference adjusting steps (v_sample + Grid::adjusted + "
+                      f"weighted_estimate) of 8D f4 at maxcalls={maxcalls:.0e} (m={m}, p={p}) after 1 untimed, "
                       f"{threads} threads, {total:.2f} s"}
 
 
-def time_to_epsrel(M, ctx):
-    """Time-to-target-relative-error (BASELINE metric, config 2) for 8D f5 at
-    tau_rel 1e-3: GPU integrate() (both streams) vs the reference integrate()
-    on host cores.  Seed 1 is reported in full (the compat stream reaches the
-    reference's estimate bit for bit); seeds 0..9 give medians, since whether
-    a given seed passes the chi^2 gate early is luck on any stream."""
+def time_to_epsrel(M, ctx, runs: int = 2, cpu_budget_s: float = 120.0):
+    """Time-to-target-relative-error, BASELINE config 2: the 8D suite f1..f6,
+    the reference tool's sweep schedule (tools/mcubes_bench.cpp:145-165:
+    tau_rel from 1e-3, divided by 5 per level, `runs` seeds per level, stop
+    tightening once fewer than half converge) with the acceptance protocol
+    (maxcalls 1e7, itmax 30, ita 10, n_bins 50).  Per level: GPU integrate()
+    on both streams and the reference integrate() on all host cores, same
+    seeds; the compat stream reaches the reference's estimates bit for bit
+    (+-*/ integrands) or to the libdevice ulp (the others).  The CPU legs stop
+    once they have used cpu_budget_s."""
     import oracle as O
     import torch
 
-    d, maxcalls, tau = 8, 10 ** 7, 1e-3
-    f = M.make_suite_integrand(5, d)
+    d, maxcalls, itmax, ita = 8, 10 ** 7, 30, 10
+    threads = os.cpu_count() or 1
+    have_cpu = O.ref_available()
+    cpu_used = 0.0
 
-    def cfg(seed, rng):
-        return M.RunConfig(dims=d, maxcalls=maxcalls, itmax=30, ita=10, tau_rel=tau, seed=seed, lower=[0.0] * d,
-                           upper=[1.0] * d, rng=rng)
+    def cfg(seed, tau, rng):
+        return M.RunConfig(dims=d, maxcalls=maxcalls, itmax=itmax, ita=ita, tau_rel=tau, seed=seed,
+                           lower=[0.0] * d, upper=[1.0] * d, rng=rng)
 
-    def gpu(seed, rng):
+    def gpu(f, seed, tau, rng):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = M.integrate(f, cfg(seed, rng), ctx=ctx)
+        r = M.integrate(f, cfg(seed, tau, rng), ctx=ctx)
         return r, 1e3 * (time.perf_counter() - t0)
 
-    M.integrate(f, cfg(1, "compat"), ctx=ctx)  # warm
-    M.integrate(f, cfg(1, "philox"), ctx=ctx)
-    r, gpu_ms = gpu(1, "compat")
-    out = {"integrand": "f5", "dims": d, "maxcalls": maxcalls, "tau_rel": tau, "itmax": 30, "ita": 10, "seed": 1,
-           "gpu_ms": gpu_ms, "gpu_iterations": r.iterations_used, "gpu_converged": r.converged,
-           "gpu_estimate": r.estimate, "gpu_sigma": r.sigma, "gpu_rng": "compat (same estimate bits as the CPU)"}
-    seeds = range(10)
-    runs = {rng: [gpu(s, rng) for s in seeds] for rng in ("compat", "philox")}
-    for rng, rr in runs.items():
-        out[f"median10_{rng}_gpu_ms"] = statistics.median(ms for _, ms in rr)
-        out[f"median10_{rng}_iterations"] = statistics.median(x.iterations_used for x, _ in rr)
-        out[f"converged10_{rng}"] = sum(x.converged for x, _ in rr)
-    if O.ref_available():
-        threads = os.cpu_count() or 1
-
-        def cpu(seed):
-            t0 = time.perf_counter()
-            o = O.integrate("ref", 5, None, d, 50, maxcalls, 30, 10, tau, 1.5, 1.5, seed, 0, [0.0] * d, [1.0] * d,
-                            workers=threads)
-            return o, 1e3 * (time.perf_counter() - t0)
-
-        o, cms = cpu(1)
-        out.update(cpu_ms=cms, cpu_iterations=o["iterations_used"], cpu_converged=o["converged"],
-                   cpu_estimate=o["estimate"], cpu_sigma=o["sigma"], cpu_threads=threads)
-        cr = [cpu(s) for s in seeds]
-        out["median10_cpu_ms"] = statistics.median(ms for _, ms in cr)
-        out["median10_cpu_iterations"] = statistics.median(x["iterations_used"] for x, _ in cr)
-        out["converged10_cpu"] = sum(x["converged"] for x, _ in cr)
-    return out
+    rows = []
+    for fam in range(1, 7):
+        f = M.make_suite_integrand(fam, d)
+        gpu(f, 1, 1e-3, "compat")  # warm (loads this integrand's kernels)
+        gpu(f, 1, 1e-3, "philox")
+        tau, level = 1e-3, 0
+        live = {"compat": True, "philox": True, "cpu": have_cpu}
+        while any(live.values()) and tau >= 1e-9:
+            seeds = [1 + level * runs + i for i in range(runs)]
+            row = {"integrand": f"f{fam}", "tau_rel": tau, "seeds": seeds}
+            for rng in ("compat", "philox"):
+                if not live[rng]:
+                    continue
+                rr = [gpu(f, sd, tau, rng) for sd in seeds]
+                conv = sum(r.converged for r, _ in rr)
+                row[f"gpu_{rng}"] = {"median_ms": statistics.median(ms for _, ms in rr), "converged": conv,
+                                     "iterations": [r.iterations_used for r, _ in rr],
+                                     "estimates": [r.estimate for r, _ in rr], "sigmas": [r.sigma for r, _ in rr]}
+                live[rng] = conv * 2 >= runs
+            if live["cpu"] and cpu_used < cpu_budget_s:
+                cr = []
+                for sd in seeds:
+                    t0 = time.perf_counter()
+                    o = O.integrate("ref", fam, None, d, 50, maxcalls, itmax, ita, tau, 1.5, 1.5, sd, 0,
+                                    [0.0] * d, [1.0] * d, workers=threads)
+                    cr.append((o, 1e3 * (time.perf_counter() - t0)))
+                cpu_used += sum(ms for _, ms in cr) / 1e3
+                conv = sum(o["converged"] for o, _ in cr)
+                row["cpu_reference"] = {"median_ms": statistics.median(ms for _, ms in cr), "converged": conv,
+                                        "iterations": [o["iterations_used"] for o, _ in cr],
+                                        "estimates": [o["estimate"] for o, _ in cr],
+                                        "sigmas": [o["sigma"] for o, _ in cr], "threads": threads}
+                live["cpu"] = conv * 2 >= runs
+                if "gpu_compat" in row:
+                    g = row["gpu_compat"]
+                    row["compat_same_iterations"] = g["iterations"] == row["cpu_reference"]["iterations"]
+                    row["compat_estimates_bitwise"] = g["estimates"] == row["cpu_reference"]["estimates"]
+                    row["speedup_compat"] = row["cpu_reference"]["median_ms"] / g["median_ms"]
+                if "gpu_philox" in row:
+                    g = row["gpu_philox"]
+                    row["philox_within_3_combined_sigma"] = all(
+                        abs(a - b) <= 3 * math.hypot(sa, sb) for a, b, sa, sb in
+                        zip(g["estimates"], row["cpu_reference"]["estimates"], g["sigmas"],
+                            row["cpu_reference"]["sigmas"]))
+                    row["speedup_philox"] = row["cpu_reference"]["median_ms"] / g["median_ms"]
+            elif live["cpu"]:
+                row["cpu_reference"] = "skipped: CPU budget spent"
+                live["cpu"] = False
+            rows.append(row)
+            tau /= 5.0
+            level += 1
+    return {"protocol": f"8D f1..f6, maxcalls 1e7, itmax 30, ita 10; tau 1e-3 / 5^k, {runs} seeds per level, "
+                        "a stream stops tightening once < 50% converge (mcubes_bench.cpp:145-165)",
+            "cpu_threads": threads, "cpu_seconds": cpu_used, "levels": rows}
 
 
 def time_to_epsrel_dist(M, ctx, dist, dev, rank, transport="collective"):
@@ -632,7 +667,10 @@ def main():
     ap.add_argument("--maxcalls", type=int, default=MAXCALLS)
     ap.add_argument("--rng", choices=["philox", "compat"], default="philox",
                     help="philox = the north-star stream (headline); compat = the reference's stream, bit-exact")
-    ap.add_argument("--no-compat", action="store_true", help="skip the secondary compat-stream measurement")
+    ap.add_argument("--bins", choices=["r24", "exact"], default="r24",
+                    help="philox: contribution addends rounded to 24 significant bits (headline) or exact")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary lines (exact bins, compat stream, maxcalls 1e10)")
     ap.add_argument("--transport", choices=["collective", "peer"], default="collective",
                     help="N > 1: exchange through an NCCL all-reduce, or K1 writing every rank's buffer over "
                          "peer memory (CUDA IPC over NVLink)")

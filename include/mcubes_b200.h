@@ -29,8 +29,10 @@
 extern "C" {
 #endif
 
-#define MCB_ABI_VERSION 1
+#define MCB_ABI_VERSION 2
 #define MCB_XWORDS 67 /* u64 words per exact accumulator in the exchange buffer */
+#define MCB_XHEADER 3 /* u64 count words ahead of the accumulators: overflowed addends, finite
+                         samples (device-counted; the write count), non-finite samples */
 
 enum mcb_status {
   MCB_OK = 0,
@@ -66,7 +68,12 @@ enum mcb_integrand_id {
 enum mcb_bin_update { MCB_BIN_ALL_AXES = 0, MCB_BIN_AXIS0_ONLY = 1, /* sampler.hpp:51-54 */
                       MCB_BIN_NONE = 2 /* frozen iteration (mcb_v_sample_philox only) */ };
 enum mcb_variant { MCB_VARIANT_MCUBES = 0, MCB_VARIANT_MCUBES1D = 1 }; /* driver.hpp:23 */
-enum mcb_rng { MCB_RNG_COMPAT = 0, MCB_RNG_PHILOX = 1 };
+/* Sample stream and bin precision: COMPAT = the reference's keyed SplitMix
+ * stream and arithmetic order with exact bins (bitwise the reference);
+ * PHILOX = the north-star Philox4x32-10 stream, bins summed from (f J)^2
+ * rounded to 24 significant bits; PHILOX_EXACT = the Philox stream with exact
+ * bins (the reference's ExactBins precision). */
+enum mcb_rng { MCB_RNG_COMPAT = 0, MCB_RNG_PHILOX = 1, MCB_RNG_PHILOX_EXACT = 2 };
 
 typedef struct mcb_ctx mcb_ctx;
 typedef struct mcb_run mcb_run;
@@ -161,6 +168,14 @@ int mcb_v_sample_philox(mcb_ctx* ctx, const mcb_integrand* f, uint32_t dims, uin
                         int32_t bin_update, double* estimate, double* variance, double* contrib,
                         uint64_t* writes);
 
+/* ---- v_sample on any stream (mcb_rng: COMPAT, PHILOX, PHILOX_EXACT);
+ * bin_update as mcb_v_sample_philox.  *writes is the device-counted number of
+ * contribution deposits (sampler.hpp:116-119). ---- */
+int mcb_v_sample_rng(mcb_ctx* ctx, const mcb_integrand* f, int32_t rng, uint32_t dims, uint32_t n_bins,
+                     const double* lower, const double* upper, const double* edges, uint64_t m, uint64_t s,
+                     uint64_t p, uint64_t seed, uint64_t iteration, int32_t bin_update, double* estimate,
+                     double* variance, double* contrib, uint64_t* writes);
+
 /* ---- grid adaptation on the device: Grid::adjusted / adjusted_symmetric
  * (grid.hpp:104-146, 232-297).  symmetric != 0 reads contrib row 0 only. ---- */
 int mcb_grid_adjust(mcb_ctx* ctx, uint32_t dims, uint32_t n_bins, const double* lower,
@@ -198,9 +213,10 @@ int mcb_integrate_resume(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config*
 int mcb_run_create(mcb_ctx* ctx, const mcb_integrand* f, const mcb_config* cfg, mcb_run** out);
 int mcb_run_destroy(mcb_run* run);
 /* Exchange buffer length (u64 words) for iteration it (1-based; 0 = the
- * largest).  Word 0 counts non-finite samples, then MCB_XWORDS words per
- * accumulator (est+, est-, var, bins); all-reducing the first
- * mcb_run_exchange_words(run, it) words covers iteration it. */
+ * largest).  MCB_XHEADER count words (overflowed exact addends, finite
+ * samples, non-finite samples), then MCB_XWORDS words per accumulator (est+,
+ * est-, var, bins); all-reducing the first mcb_run_exchange_words(run, it)
+ * words covers iteration it. */
 uint64_t mcb_run_exchange_words(const mcb_run* run, uint32_t it);
 /* Use a caller-owned DEVICE buffer (>= max exchange words) for the exchange. */
 int mcb_run_set_exchange(mcb_run* run, void* device_ptr);

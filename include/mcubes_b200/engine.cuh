@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -174,6 +175,8 @@ inline Shape make_shape(std::uint32_t dims, std::uint32_t nb, std::uint64_t m, s
   if (s == 0) throw std::invalid_argument("v_sample: batch size must be >= 1");
   const std::uint64_t g = exact_root(m, dims);
   if (g == 0) throw std::invalid_argument("v_sample: m must be a perfect d-th power of the cube count");
+  if (p >= (std::uint64_t{1} << 32))  // K1 keys samples by a 32-bit index (Philox counter word, Welford count)
+    throw std::invalid_argument("B200 path: p must be < 2^32 samples per cube");
   if (dims > static_cast<std::uint32_t>(kMaxDims))
     throw std::invalid_argument("B200 path: dims must be <= " + std::to_string(kMaxDims));
   Shape sh;
@@ -233,9 +236,14 @@ class Context {
   /// Number of kernels this context enqueued (our own kernels only).
   std::uint64_t launches = 0;
 
-  DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var, scalars, point;
+  /// Scratch of the standalone calls (v_sample, v_sample_no_adjust,
+  /// Grid::adjusted); a Run owns its own buffers (mcubes.cuh Run::Bufs).
+  DevBuf<double> edges, lower, upper, contrib, scalars, point;
   DevBuf<unsigned long long> words, err_key;
-  DevBuf<RunState> state;
+  /// The grid the next K1 / point-kernel launch reads (device edges, lower
+  /// bounds), bound by the caller right before it enqueues the launch.
+  const double* grid_edges = nullptr;
+  const double* grid_lower = nullptr;
   DevBuf<unsigned int> counter;  ///< finish-kernel last-block counter (self-resetting)
   DevBuf<unsigned int> peer_counter;  ///< K1 last-block counter of the peer-memory exchange (self-resetting)
   /// Peer-memory exchange of the launch being enqueued (npeers == 0: off);
@@ -293,7 +301,7 @@ struct Launch {
 };
 
 /// Cells per axis in K1's shared histogram for a stream kind.
-constexpr std::uint32_t partial_bins(RngKind r, std::uint32_t nb) { return nb + (r == RngKind::philox ? 1u : 0u); }
+constexpr std::uint32_t partial_bins(RngKind r, std::uint32_t nb) { return nb + (philox_stream(r) ? 1u : 0u); }
 
 /// The work-index -> cube map of K1 (see vsample_kernel): whole rows along
 /// axis 0 once there are enough of them.
@@ -361,8 +369,9 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   const int walkers = threads;  // threads that walk cubes
 
   SampleArgs a{};
-  a.edges = ctx.edges.get();
-  a.lower = ctx.lower.get();
+  if (!ctx.grid_edges || !ctx.grid_lower) throw std::invalid_argument("K1: no grid bound to the context");
+  a.edges = ctx.grid_edges;
+  a.lower = ctx.grid_lower;
   a.dims = sh.dims;
   a.nb = sh.nb;
   a.bin_axes = bin_axes;
@@ -431,8 +440,9 @@ template <class F, int D, RngKind R>
 void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_root, std::uint64_t t,
                   std::uint64_t k, double* out_x, double* out_fx) {
   SampleArgs a{};
-  a.edges = ctx.edges.get();
-  a.lower = ctx.lower.get();
+  if (!ctx.grid_edges || !ctx.grid_lower) throw std::invalid_argument("K1: no grid bound to the context");
+  a.edges = ctx.grid_edges;
+  a.lower = ctx.grid_lower;
   a.dims = sh.dims;
   a.nb = sh.nb;
   a.m = sh.m;
@@ -514,7 +524,7 @@ inline int adjust_warps(std::uint32_t dims, std::uint32_t nb, int max_smem) {
 /// an epilogue, also grid adaptation + weighted estimate + convergence.
 inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes, unsigned long long* words,
                           double* est, double* var, double* contrib, const int* stop, const EpilogueArgs* epi,
-                          bool zero_words = false) {
+                          bool zero_words = false, unsigned long long* counts = nullptr) {
   RoundArgs r{};
   r.words = words;
   r.dims = sh.dims;
@@ -524,6 +534,7 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   r.est = est;
   r.var = var;
   r.contrib = contrib;
+  r.counts = counts;
   r.stop = stop;
   r.zero_words = (zero_words && epi) ? 1 : 0;
   if (epi && ctx.peer.npeers) {
@@ -542,10 +553,11 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
     smem = e.adj_par ? par
                      : sizeof(double) * (staged + static_cast<std::size_t>(e.adj_warps) * kAdjustScratch * sh.nb);
   }
-  thread_local std::size_t attr_smem = 0;
-  if (smem > 48 * 1024 && smem > attr_smem) {
+  // the raised limit is a per-device function attribute: cache it per device
+  thread_local std::map<int, std::size_t> attr_smem;
+  if (smem > 48 * 1024 && smem > attr_smem[ctx.device()]) {
     MCB_CUDA(cudaFuncSetAttribute(finish_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_smem = smem;
+    attr_smem[ctx.device()] = smem;
   }
   unsigned int* counter = ctx.counter.get();
   if (!counter) {

@@ -25,11 +25,13 @@ namespace mcubes::gpu {
 struct RunState {
   int stop;
   int converged;
-  int failed;  ///< a non-finite sample was seen (err_key holds the first one)
+  int failed;  ///< 1: a non-finite sample was seen (err_key holds the first one); 2: an exact addend overflowed
   std::uint32_t iterations_used;
   std::uint32_t failed_iteration;
   std::uint32_t pad;
   double estimate, sigma, chi2_dof;
+  unsigned long long samples;     ///< finite samples taken over the run (device-counted by K1)
+  unsigned long long bin_writes;  ///< contribution deposits over the run (samples * bin_axes per iteration)
 };
 
 /// Exchange-buffer slots: est+, est-, var, then bin_axes*nb bins.
@@ -479,12 +481,14 @@ MCB_HD bool converged_dev(double est, double sigma, double chi2, double tau, dou
 
 // ------------------------------------------------------------------ finish (K3b + K4)
 struct RoundArgs {
-  unsigned long long* words;  ///< [exchange_accs][kXWords], words[-1] the non-finite count; zeroed by the epilogue when zero_words
+  unsigned long long* words;  ///< [exchange_accs][kXWords]; words[-2] the finite-sample count, words[-1] the
+                              ///< non-finite count; zeroed by the epilogue when zero_words
   std::uint32_t dims, nb, bin_axes;
   double md2;        ///< double(m) * double(m)  (sampler.hpp:330-331)
   double* est;       ///< 1 double
   double* var;       ///< 1 double
   double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
+  unsigned long long* counts;  ///< nullable: {samples, writes, overflowed addends} of this iteration (no epilogue)
   const int* stop;
   int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K1 flush (integrate loop)
   const unsigned long long* wait_flags;  ///< peer-memory exchange: wait until these nwait flags reach wait_value
@@ -562,7 +566,14 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
       if (r.zero_words && c < nbins) zero_acc(w, 1);
     }
   }
-  if (!with_epilogue) return;
+  if (!with_epilogue) {
+    if (r.counts && blockIdx.x == 0 && threadIdx.x == 0) {
+      r.counts[0] = r.words[-2];
+      r.counts[1] = r.words[-2] * r.bin_axes;
+      r.counts[2] = r.words[-3];
+    }
+    return;
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) MCB_FIN_STAMP_MAX(1);
@@ -587,12 +598,18 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   RunState* st = e.st;
   // words[-1] counts non-finite samples over every rank's slice (exchanged
   // with the words), err_key holds this rank's first one
-  const unsigned long long nonfinite = r.words[-1];
+  const unsigned long long nonfinite = r.words[-1], samples = r.words[-2], overflow = r.words[-3];
   __syncthreads();
-  if (threadIdx.x == 0 && r.zero_words) r.words[-1] = 0ull;
-  if (*e.err_key != ~0ull || nonfinite != 0) {  // NonFiniteSample: abort the run (driver.hpp:231-241 propagate)
+  if (threadIdx.x == 0) {
+    st->samples += samples;  // the write count the reference reports (sampler.hpp:116-119, driver.hpp:242-244)
+    st->bin_writes += samples * r.bin_axes;
+    if (r.zero_words) r.words[-1] = r.words[-2] = r.words[-3] = 0ull;
+  }
+  // NonFiniteSample (1) or an overflowed exact addend (2, ExactSum's
+  // invalid_argument): abort the run (driver.hpp:231-241 propagate)
+  if (*e.err_key != ~0ull || nonfinite != 0 || overflow != 0) {
     if (threadIdx.x == 0) {
-      st->failed = 1;
+      st->failed = (*e.err_key != ~0ull || nonfinite != 0) ? 1 : 2;
       st->failed_iteration = e.it;
       st->stop = 1;
       if (e.host_flags) e.host_flags[e.it - 1] = 2;

@@ -137,6 +137,8 @@ struct Digits2 {
 };
 
 inline constexpr int kBinDrop = 29;  ///< significand bits dropped: 53 - 24
+/// Smallest double that RN24 (round_bin_bits) rounds up to 2^1024.
+inline constexpr double kR24Max = 0x1.ffffffp+1023;
 
 MCB_HD std::uint64_t round_bin_bits(std::uint64_t bits) {
   return (bits + (1ull << (kBinDrop - 1))) & ~((1ull << kBinDrop) - 1);  // carries into the exponent
@@ -234,6 +236,44 @@ __device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N],
       const std::uint32_t a = base[j] + static_cast<std::uint32_t>(j) * kRow;
       if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a + 8, 1u) == 0xffffffffu) carry_up_s(a + 12, end);
     }
+  }
+}
+#endif
+
+#ifdef __CUDACC__
+/// add_digits_s (three words, the exact addend) with the axis row offsets
+/// j*kRow as immediates, as add_digits2_rows: the Philox stream with exact bins.
+template <int N, std::uint32_t kRow>
+__device__ __forceinline__ void add_digits_rows(const std::uint32_t (&base)[N], std::uint32_t end,
+                                                const Digits& dg) {
+  std::uint32_t t1[N], u[N];
+  [&]<std::size_t... J>(std::index_sequence<J...>) {
+    ((void)[&] {
+      const std::uint32_t o = atoms_add_at<static_cast<std::uint32_t>(J) * kRow>(base[J], dg.d0);
+      asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %2, %3;\n\taddc.cc.u32 %0, %4, 0;\n\taddc.u32 %1, %5, 0;\n\t}"
+          : "=r"(t1[J]), "=r"(u[J])
+          : "r"(o), "r"(dg.d0), "r"(dg.d1), "r"(dg.d2));
+    }(), ...);
+  }(std::make_index_sequence<N>{});
+  std::uint32_t t2[N];
+  [&]<std::size_t... J>(std::index_sequence<J...>) {
+    ((void)[&] {
+      const std::uint32_t o = atoms_add_at<static_cast<std::uint32_t>(J) * kRow + 4u>(base[J], t1[J]);
+      asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}"
+          : "=r"(t2[J]) : "r"(o), "r"(t1[J]), "r"(u[J]));
+    }(), ...);
+  }(std::make_index_sequence<N>{});
+  std::uint32_t ripple = 0;
+  [&]<std::size_t... J>(std::index_sequence<J...>) {
+    ((void)[&] {
+      const std::uint32_t o = atoms_add_at<static_cast<std::uint32_t>(J) * kRow + 8u>(base[J], t2[J]);
+      asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, %0, %0;\n\t}" : "+r"(ripple) : "r"(o), "r"(t2[J]));
+    }(), ...);
+  }(std::make_index_sequence<N>{});
+  if (ripple) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(base[j] + static_cast<std::uint32_t>(j) * kRow + 12, end);
   }
 }
 #endif

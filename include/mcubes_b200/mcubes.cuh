@@ -152,6 +152,16 @@ IntegrandOps make_ops(const F& f) {
   return ops;
 }
 
+/// make_ops for a stream chosen at run time.
+template <DeviceIntegrand F>
+IntegrandOps make_ops_for(const F& f, RngKind r) {
+  switch (r) {
+    case RngKind::philox: return make_ops<F, RngKind::philox>(f);
+    case RngKind::philox_exact: return make_ops<F, RngKind::philox_exact>(f);
+    default: return make_ops<F, RngKind::compat>(f);
+  }
+}
+
 /// Per-iteration key: the reference's iteration root (rng.hpp:47-50); the
 /// Philox stream uses the same 64-bit value as its key.
 inline std::uint64_t iteration_key(std::uint64_t seed, std::uint64_t it) { return rng::iteration_root(seed, it); }
@@ -175,6 +185,10 @@ inline void download(Context& ctx, double* host, const double* dev, std::size_t 
   hx.resize(sh.dims);
   throw NonFiniteSample(std::move(hx), fx);
 }
+
+/// An exact addend ((f J)^2, a cube's sum or variance) overflowed to inf:
+/// the reference's ExactSum::add throws this (exact_sum.hpp:34).
+[[noreturn]] inline void throw_overflow() { throw std::invalid_argument("ExactSum: non-finite addend"); }
 
 }  // namespace gpu
 
@@ -374,6 +388,8 @@ namespace gpu {
 /// One iteration on the GPU for a host grid.  bin_axes: 0 frozen, 1 axis0, d all.
 struct SampleResult {
   double est = 0, var = 0;
+  std::uint64_t samples = 0;  ///< finite samples taken, counted on the device
+  std::uint64_t writes = 0;   ///< contribution deposits (samples * bin_axes; 0 when frozen)
   std::vector<double> contrib;
 };
 
@@ -385,33 +401,41 @@ inline SampleResult sample_once(Context& ctx, const IntegrandOps& ops, const Gri
   const std::size_t n = std::size_t{grid.dims()} * grid.n_bins();
   upload(ctx, ctx.edges, grid.raw_edges().data(), n);
   upload(ctx, ctx.lower, grid.lowers().data(), grid.dims());
+  ctx.grid_edges = ctx.edges.get();
+  ctx.grid_lower = ctx.lower.get();
   unsigned long long* err = ctx.err_key.ensure(1);
   MCB_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx.stream()));
   const std::uint64_t root = iteration_key(seed, iteration);
-  // exchange buffer: the non-finite count word, then the accumulator words
-  const std::size_t nwords = 1 + static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords;
+  // exchange buffer: the sample and non-finite count words, then the accumulator words
+  const std::size_t nwords = kXHeader + static_cast<std::size_t>(exchange_accs(bin_axes, sh.nb)) * kXWords;
   unsigned long long* xbuf = ctx.words.ensure(nwords);
   MCB_CUDA(cudaMemsetAsync(xbuf, 0, sizeof(unsigned long long) * nwords, ctx.stream()));
-  unsigned long long* words = xbuf + 1;
+  unsigned long long* words = xbuf + kXHeader;
   (void)ops.k1(ctx, sh, bin_axes, root, 0, m, nullptr, err, words);  // K1 flushes straight into the words
-  double* sc = ctx.scalars.ensure(2);
+  double* sc = ctx.scalars.ensure(5);  // est, var, then the {samples, writes, overflowed} counts
+  auto* counts = reinterpret_cast<unsigned long long*>(sc + 2);
   double* contrib = bin_axes ? ctx.contrib.ensure(n) : nullptr;
-  launch_finish(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr, nullptr);
+  launch_finish(ctx, sh, bin_axes, words, sc, sc + 1, contrib, nullptr, nullptr, false, counts);
   // results back through pinned staging
   auto* pin = reinterpret_cast<double*>(ctx.pinned());
-  const std::size_t nd = 2 + (bin_axes ? n : 0);
+  const std::size_t nd = 5 + (bin_axes ? n : 0);
   if ((nd + 1) * sizeof(double) > Context::kPinnedBytes) throw std::invalid_argument("grid too large");
-  MCB_CUDA(cudaMemcpyAsync(pin, sc, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx.stream()));
-  if (bin_axes) MCB_CUDA(cudaMemcpyAsync(pin + 2, contrib, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream()));
+  MCB_CUDA(cudaMemcpyAsync(pin, sc, sizeof(double) * 5, cudaMemcpyDeviceToHost, ctx.stream()));
+  if (bin_axes) MCB_CUDA(cudaMemcpyAsync(pin + 5, contrib, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream()));
   MCB_CUDA(cudaMemcpyAsync(pin + nd, err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx.stream()));
   ctx.sync();
   unsigned long long key;
   std::memcpy(&key, pin + nd, sizeof key);
   if (key != ~0ull) throw_nonfinite(ctx, ops, sh, root, key);
+  unsigned long long overflow;
+  std::memcpy(&overflow, pin + 4, 8);
+  if (overflow) throw_overflow();
   SampleResult r;
   r.est = pin[0];
   r.var = pin[1];
-  if (bin_axes) r.contrib.assign(pin + 2, pin + 2 + n);
+  std::memcpy(&r.samples, pin + 2, 8);
+  std::memcpy(&r.writes, pin + 3, 8);
+  if (bin_axes) r.contrib.assign(pin + 5, pin + 5 + n);
   return r;
 }
 
@@ -427,7 +451,7 @@ SampleOutcome v_sample(const F& f, const Grid& grid, std::uint64_t m, std::uint6
   (void)max_threads;
   const std::uint32_t bin_axes = mode == BinUpdate::all_axes ? grid.dims() : 1;
   auto r = gpu::sample_once(gpu::default_context(), gpu::make_ops(f), grid, m, s, p, seed, iteration, bin_axes);
-  return {r.est, r.var, BinAccumulator(grid.dims(), grid.n_bins(), std::move(r.contrib), m * p * bin_axes)};
+  return {r.est, r.var, BinAccumulator(grid.dims(), grid.n_bins(), std::move(r.contrib), r.writes)};
 }
 
 /// Frozen-grid iteration (sampler.hpp:339-349), on the GPU.
@@ -599,13 +623,13 @@ class Run {
     ctx_.activate();
     const Grid g0(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper);
     const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
-    ctx_.contrib.ensure(n);
-    ctx_.hist_est.ensure(cfg_.itmax);
-    ctx_.hist_var.ensure(cfg_.itmax);
-    ctx_.state.ensure(1);
-    ctx_.err_key.ensure(1);
-    xbuf_ = ctx_.words.ensure(exchange_words(cfg_.dims));
-    words_ = xbuf_ + 1;
+    b_.contrib.ensure(n);
+    b_.hist_est.ensure(cfg_.itmax);
+    b_.hist_var.ensure(cfg_.itmax);
+    b_.state.ensure(1);
+    b_.err_key.ensure(1);
+    xbuf_ = b_.words.ensure(exchange_words(cfg_.dims));
+    words_ = xbuf_ + kXHeader;
     if (sizeof(double) * (n + 2 * cfg_.dims) <= Context::kPinnedBytes) {
       // one launch: the kernel reads the staged grid from pinned host memory
       // and zeroes the state and the exchange words
@@ -616,18 +640,18 @@ class Run {
       std::memcpy(pin + n + cfg_.dims, cfg_.upper.data(), sizeof(double) * cfg_.dims);
       const auto nw = static_cast<std::uint32_t>(exchange_words(cfg_.dims));
       launch_pdl(run_init_kernel<0>, std::max<std::uint32_t>(1, (nw + 255) / 256), 256, 0, ctx_.stream(),
-                 static_cast<const double*>(pin), static_cast<std::uint32_t>(n), cfg_.dims, ctx_.edges.ensure(n),
-                 ctx_.lower.ensure(cfg_.dims), ctx_.upper.ensure(cfg_.dims), ctx_.state.get(), ctx_.err_key.get(),
+                 static_cast<const double*>(pin), static_cast<std::uint32_t>(n), cfg_.dims, b_.edges.ensure(n),
+                 b_.lower.ensure(cfg_.dims), b_.upper.ensure(cfg_.dims), b_.state.get(), b_.err_key.get(),
                  xbuf_, nw);
       ++ctx_.launches;
       ctx_.staging_recorded();
       words_clean_ = true;
     } else {
-      upload(ctx_, ctx_.edges, g0.raw_edges().data(), n);
-      upload(ctx_, ctx_.lower, cfg_.lower.data(), cfg_.dims);
-      upload(ctx_, ctx_.upper, cfg_.upper.data(), cfg_.dims);
-      MCB_CUDA(cudaMemsetAsync(ctx_.state.get(), 0, sizeof(RunState), ctx_.stream()));
-      MCB_CUDA(cudaMemsetAsync(ctx_.err_key.get(), 0xff, sizeof(unsigned long long), ctx_.stream()));
+      upload(ctx_, b_.edges, g0.raw_edges().data(), n);
+      upload(ctx_, b_.lower, cfg_.lower.data(), cfg_.dims);
+      upload(ctx_, b_.upper, cfg_.upper.data(), cfg_.dims);
+      MCB_CUDA(cudaMemsetAsync(b_.state.get(), 0, sizeof(RunState), ctx_.stream()));
+      MCB_CUDA(cudaMemsetAsync(b_.err_key.get(), 0xff, sizeof(unsigned long long), ctx_.stream()));
       zero_exchange();
     }
   }
@@ -647,7 +671,7 @@ class Run {
     if (n > cfg_.itmax) throw std::invalid_argument("resume: more completed iterations than itmax");
     for (std::uint32_t i = 0; i < n; ++i)
       if (history[i].index != i + 1) throw std::invalid_argument("resume: history indices must be 1..n");
-    upload(ctx_, ctx_.edges, grid.raw_edges().data(), std::size_t{cfg_.dims} * cfg_.n_bins);
+    upload(ctx_, b_.edges, grid.raw_edges().data(), std::size_t{cfg_.dims} * cfg_.n_bins);
     RunState st{};
     if (n) {
       std::vector<double> e(n), v(n);
@@ -655,16 +679,22 @@ class Run {
         e[i] = history[i].estimate;
         v[i] = history[i].variance;
       }
-      upload(ctx_, ctx_.hist_est, e.data(), n);
-      upload(ctx_, ctx_.hist_var, v.data(), n);
+      upload(ctx_, b_.hist_est, e.data(), n);
+      upload(ctx_, b_.hist_var, v.data(), n);
       const Combined c = weighted_estimate(history);  // driver.hpp:246-252, as the device epilogue does
       st.iterations_used = n;
+      // a checkpoint carries no counts: the completed iterations are credited
+      // with the samples and deposits a full iteration takes
+      for (std::uint32_t i = 1; i <= n; ++i) {
+        st.samples += sp_.m * sp_.p;
+        st.bin_writes += sp_.m * sp_.p * bin_axes(i);
+      }
       st.estimate = c.estimate;
       st.sigma = c.sigma;
       st.chi2_dof = c.chi2_dof;
       if (check_convergence(c, cfg_)) st.converged = st.stop = 1;
     }
-    MCB_CUDA(cudaMemcpyAsync(ctx_.state.get(), &st, sizeof st, cudaMemcpyHostToDevice, ctx_.stream()));
+    MCB_CUDA(cudaMemcpyAsync(b_.state.get(), &st, sizeof st, cudaMemcpyHostToDevice, ctx_.stream()));
     ctx_.sync();  // the host-side state copy above must land before it goes out of scope
     return n + 1;
   }
@@ -675,16 +705,17 @@ class Run {
     if (it > cfg_.ita) return 0;
     return cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims;
   }
-  /// Exchange buffer length (u64 words): one word counting non-finite samples
-  /// (so every rank learns of a failure in any rank's slice), then the
+  /// Exchange buffer length (u64 words): the kXHeader count words -- finite
+  /// samples taken (device-counted: the write count) and non-finite samples
+  /// (so every rank learns of a failure in any rank's slice) -- then the
   /// accumulators.  An all-reduce of the first exchange_words_for(it) words
   /// covers iteration it.
   std::size_t exchange_words(std::uint32_t) const {
-    return 1 + static_cast<std::size_t>(exchange_accs(cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims,
+    return kXHeader + static_cast<std::size_t>(exchange_accs(cfg_.variant == Variant::mcubes1d ? 1u : cfg_.dims,
                                                       cfg_.n_bins)) * kXWords;
   }
   std::size_t exchange_words_for(std::uint32_t it) const {
-    return 1 + static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
+    return kXHeader + static_cast<std::size_t>(exchange_accs(bin_axes(it), cfg_.n_bins)) * kXWords;
   }
   unsigned long long* exchange() const { return xbuf_; }
   void zero_exchange() {
@@ -698,11 +729,11 @@ class Run {
   /// tensor the caller all-reduces).  It is zeroed here; finish() leaves it
   /// zeroed for the next iteration.
   void set_exchange(unsigned long long* p) {
-    xbuf_ = p ? p : ctx_.words.get();
-    words_ = xbuf_ + 1;
+    xbuf_ = p ? p : b_.words.get();
+    words_ = xbuf_ + kXHeader;
     zero_exchange();
   }
-  const int* stop_flag() const { return &ctx_.state.get()->stop; }
+  const int* stop_flag() const { return &b_.state.get()->stop; }
 
   /// K1 over the work slice [n0, n1) of the linear work index (default: all
   /// cubes).  Its blocks flush straight into exchange(): after sample() the
@@ -715,14 +746,16 @@ class Run {
       // adding this iteration's words into our buffer; finish() leaves each
       // buffer zeroed after reading it, and the two alternate by parity
       use_peers(it);
+      bind_grid();
       last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(),
-                      ctx_.err_key.get(), words_);
+                      b_.err_key.get(), words_);
       ctx_.peer.npeers = 0;
       last_it_ = it;
       return;
     }
     if (!words_clean_) zero_exchange();
-    last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), ctx_.err_key.get(),
+    bind_grid();
+    last_ = ops_.k1(ctx_, sh_, bin_axes(it), iteration_key(cfg_.seed, it), n0, n1, stop_flag(), b_.err_key.get(),
                     words_);
     words_clean_ = false;
     last_it_ = it;
@@ -762,29 +795,29 @@ class Run {
     if (npeers_) use_peers(it);
     const std::uint32_t ba = bin_axes(it);
     EpilogueArgs e{};
-    e.st = ctx_.state.get();
-    e.hist_est = ctx_.hist_est.get();
-    e.hist_var = ctx_.hist_var.get();
-    e.err_key = ctx_.err_key.get();
+    e.st = b_.state.get();
+    e.hist_est = b_.hist_est.get();
+    e.hist_var = b_.hist_var.get();
+    e.err_key = b_.err_key.get();
     e.it = it;
     e.adjusting = ba ? 1 : 0;
     e.tau = cfg_.tau_rel;
     e.chi2max = cfg_.chi2_dof_max;
     e.adj = AdjustArgs{cfg_.dims,       cfg_.n_bins,
-                       ctx_.lower.get(), ctx_.upper.get(),
-                       ctx_.edges.get(), ctx_.contrib.get(),
+                       b_.lower.get(), b_.upper.get(),
+                       b_.edges.get(), b_.contrib.get(),
                        cfg_.alpha,       cfg_.variant == Variant::mcubes1d ? 1 : 0,
-                       ctx_.contrib.get()};
+                       b_.contrib.get()};
     e.host_flags = host_flags_;
-    launch_finish(ctx_, sh_, ba, words_, ctx_.hist_est.get() + (it - 1), ctx_.hist_var.get() + (it - 1),
-                  ba ? ctx_.contrib.get() : nullptr, stop_flag(), &e, /*zero_words=*/true);
+    launch_finish(ctx_, sh_, ba, words_, b_.hist_est.get() + (it - 1), b_.hist_var.get() + (it - 1),
+                  ba ? b_.contrib.get() : nullptr, stop_flag(), &e, /*zero_words=*/true);
     ctx_.peer.npeers = 0;
     words_clean_ = true;  // (or the run is stopped, and reduce() is a no-op)
   }
 
   RunState state() {
     RunState st;
-    MCB_CUDA(cudaMemcpyAsync(&st, ctx_.state.get(), sizeof st, cudaMemcpyDeviceToHost, ctx_.stream()));
+    MCB_CUDA(cudaMemcpyAsync(&st, b_.state.get(), sizeof st, cudaMemcpyDeviceToHost, ctx_.stream()));
     ctx_.sync();
     return st;
   }
@@ -796,24 +829,24 @@ class Run {
   /// NonFiniteSample (the reference reports the first in serial order).
   bool failure_key(unsigned long long& key) {
     const RunState st = state();
-    MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
+    MCB_CUDA(cudaMemcpyAsync(&key, b_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
     ctx_.sync();
     return st.failed != 0;
   }
   void set_failure_key(unsigned long long key) {
-    MCB_CUDA(cudaMemcpyAsync(ctx_.err_key.get(), &key, sizeof key, cudaMemcpyHostToDevice, ctx_.stream()));
+    MCB_CUDA(cudaMemcpyAsync(b_.err_key.get(), &key, sizeof key, cudaMemcpyHostToDevice, ctx_.stream()));
     ctx_.sync();
   }
 
   /// Replace the device grid with host edges (dims*n_bins), stream-ordered.
   void set_grid(const double* host_edges) {
-    upload(ctx_, ctx_.edges, host_edges, std::size_t{cfg_.dims} * cfg_.n_bins);
+    upload(ctx_, b_.edges, host_edges, std::size_t{cfg_.dims} * cfg_.n_bins);
   }
 
   Grid grid() {
     const std::size_t n = std::size_t{cfg_.dims} * cfg_.n_bins;
     std::vector<double> e(n);
-    download(ctx_, e.data(), ctx_.edges.get(), n);
+    download(ctx_, e.data(), b_.edges.get(), n);
     ctx_.sync();
     return Grid::from_edges(cfg_.dims, cfg_.n_bins, cfg_.lower, cfg_.upper, std::move(e));
   }
@@ -831,8 +864,8 @@ class Run {
     if (staged) {
       ctx_.staging_wait();
       launch_pdl(run_collect_kernel<0>, std::max<std::uint32_t>(1, (cfg_.itmax + 255) / 256), 256, 0, ctx_.stream(),
-                 static_cast<const RunState*>(ctx_.state.get()), static_cast<const unsigned long long*>(ctx_.err_key.get()),
-                 static_cast<const double*>(ctx_.hist_est.get()), static_cast<const double*>(ctx_.hist_var.get()),
+                 static_cast<const RunState*>(b_.state.get()), static_cast<const unsigned long long*>(b_.err_key.get()),
+                 static_cast<const double*>(b_.hist_est.get()), static_cast<const double*>(b_.hist_var.get()),
                  cfg_.itmax, pin);
       ++ctx_.launches;
       ctx_.sync();
@@ -844,24 +877,28 @@ class Run {
       v.assign(hv, hv + st.iterations_used);
     } else {
       st = state();
-      MCB_CUDA(cudaMemcpyAsync(&key, ctx_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
+      MCB_CUDA(cudaMemcpyAsync(&key, b_.err_key.get(), sizeof key, cudaMemcpyDeviceToHost, ctx_.stream()));
       e.resize(st.iterations_used);
       v.resize(st.iterations_used);
       if (st.iterations_used) {
-        download(ctx_, e.data(), ctx_.hist_est.get(), st.iterations_used);
-        download(ctx_, v.data(), ctx_.hist_var.get(), st.iterations_used);
+        download(ctx_, e.data(), b_.hist_est.get(), st.iterations_used);
+        download(ctx_, v.data(), b_.hist_var.get(), st.iterations_used);
       }
       ctx_.sync();
     }
     IntegrationResult res;
     res.params = sp_;
-    if (st.failed) throw_nonfinite(ctx_, ops_, sh_, iteration_key(cfg_.seed, st.failed_iteration), key);
-    const std::uint32_t n = st.iterations_used;
-    for (std::uint32_t i = 0; i < n; ++i) {
-      res.history.push_back({e[i], v[i], i + 1});
-      res.total_samples += sp_.m * sp_.p;
-      res.bin_writes += sp_.m * sp_.p * bin_axes(i + 1);
+    if (st.failed == 2) throw_overflow();
+    if (st.failed) {
+      bind_grid();  // the failed iteration's grid (the epilogue aborted before adapting it)
+      throw_nonfinite(ctx_, ops_, sh_, iteration_key(cfg_.seed, st.failed_iteration), key);
     }
+    const std::uint32_t n = st.iterations_used;
+    for (std::uint32_t i = 0; i < n; ++i) res.history.push_back({e[i], v[i], i + 1});
+    // device-counted: every finite sample K1 took, and the deposits it made
+    // (a resumed run counts only the iterations it ran itself)
+    res.total_samples = st.samples;
+    res.bin_writes = st.bin_writes;
     res.iterations_used = n;
     res.converged = st.converged != 0;
     res.estimate = st.estimate;
@@ -872,17 +909,30 @@ class Run {
 
  private:
   Context& ctx_;
+  /// The run's own device buffers: nothing else enqueued on the context
+  /// (a standalone v_sample, Grid::adjusted, another Run, e.g. from an
+  /// observer) can replace this run's grid, state or exchange words.
+  struct Bufs {
+    DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var;
+    DevBuf<unsigned long long> words, err_key;
+    DevBuf<RunState> state;
+  } b_;
   IntegrandOps ops_;
   RunConfig cfg_;
   SetupParams sp_{};
   Shape sh_{};
+  /// K1 / the point kernel read this run's grid.
+  void bind_grid() {
+    ctx_.grid_edges = b_.edges.get();
+    ctx_.grid_lower = b_.lower.get();
+  }
   /// Point the launch at iteration it's buffers: parity it & 1, flag = it.
   void use_peers(std::uint32_t it) {
     PeerArgs& p = ctx_.peer;
     p = PeerArgs{};
     const int par = static_cast<int>(it & 1u);
     for (int q = 0; q < npeers_; ++q) {
-      p.words[q] = peer_bufs_[par][q] + 1;
+      p.words[q] = peer_bufs_[par][q] + kXHeader;
       p.flags[q] = peer_flags_[q] + rank_;
     }
     p.my_flags = peer_flags_[rank_];
@@ -890,15 +940,15 @@ class Run {
     p.flag = it;
     p.npeers = npeers_;
     xbuf_ = peer_bufs_[par][rank_];
-    words_ = xbuf_ + 1;
+    words_ = xbuf_ + kXHeader;
   }
 
   int npeers_ = 0, rank_ = 0;
   unsigned long long* peer_bufs_[2][kMaxPeers] = {};
   unsigned long long* peer_flags_[kMaxPeers] = {};
   unsigned int* peer_counter_ = nullptr;
-  unsigned long long* xbuf_ = nullptr;   ///< exchange buffer: [non-finite count][accumulator words]
-  unsigned long long* words_ = nullptr;  ///< xbuf_ + 1
+  unsigned long long* xbuf_ = nullptr;   ///< exchange buffer: [sample count][non-finite count][accumulator words]
+  unsigned long long* words_ = nullptr;  ///< xbuf_ + kXHeader
   Launch last_{};
   std::uint32_t last_it_ = 0;
   int* host_flags_ = nullptr;
@@ -925,6 +975,7 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
     std::memset(flags, 0, sizeof(int) * cfg.itmax);
     run.set_host_flags(flags);
   }
+  unsigned long long writes_before = 0;  // device-counted deposits before this iteration (observer views)
   for (std::uint32_t it = first; it <= cfg.itmax; ++it) {
     if (lookahead && it >= first + kAhead) {
       const std::uint32_t back = it - kAhead;
@@ -941,7 +992,8 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
       const IterationResult r = run.result().history.back();
       const Combined c{st.estimate, st.sigma, st.chi2_dof};
       const Grid g = run.grid();
-      observe(IterationView{it, it <= cfg.ita, r, c, g, run.params().m * run.params().p * run.bin_axes(it)});
+      observe(IterationView{it, it <= cfg.ita, r, c, g, st.bin_writes - writes_before});
+      writes_before = st.bin_writes;
       if (st.stop) break;
     }
   }
@@ -957,18 +1009,14 @@ template <gpu::DeviceIntegrand F>
 IntegrationResult integrate_resume(const F& f, const RunConfig& cfg, const Grid& grid,
                                    std::span<const IterationResult> history, const IterationObserver& observe = {}) {
   gpu::Context& ctx = gpu::default_context();
-  if (cfg.rng == gpu::RngKind::philox)
-    return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::philox>(f), cfg, observe, &grid, history);
-  return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::compat>(f), cfg, observe, &grid, history);
+  return gpu::integrate_ops(ctx, gpu::make_ops_for(f, cfg.rng), cfg, observe, &grid, history);
 }
 
 /// The full integration loop (driver.hpp:215-258), on the GPU.
 template <gpu::DeviceIntegrand F>
 IntegrationResult integrate(const F& f, const RunConfig& cfg, const IterationObserver& observe = {}) {
   gpu::Context& ctx = gpu::default_context();
-  if (cfg.rng == gpu::RngKind::philox)
-    return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::philox>(f), cfg, observe);
-  return gpu::integrate_ops(ctx, gpu::make_ops<F, gpu::RngKind::compat>(f), cfg, observe);
+  return gpu::integrate_ops(ctx, gpu::make_ops_for(f, cfg.rng), cfg, observe);
 }
 
 }  // namespace mcubes

@@ -73,7 +73,7 @@ struct SampleArgs {
   std::uint64_t stepR;                  ///< row mode: (T*A) mod R, A = A' = 1 + g + ... + g^(D-2)
   std::uint32_t round_keys[20];         ///< philox: (k0, k1) of rounds 0..9 (uniform; folded into LOP3)
   unsigned long long* words;  ///< exchange accumulators (zeroed): every block adds its nonzero words here;
-                              ///< words[-1] counts non-finite samples
+                              ///< words[-3..-1]: overflowed addends, finite and non-finite samples (kXHeader)
   std::uint32_t nb_out;       ///< n_bins of the exchange layout (the padding cell folds into bin nb_out-1)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
@@ -353,9 +353,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   MCB_K1_STAMP(0, atomicMin)
   MCB_K1_STAMP(1, atomicMax)
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned int nonfinite_s;  // this block's non-finite samples (flushed with the words)
+  __shared__ unsigned int nonfinite_s;        // this block's non-finite samples (flushed with the words)
+  __shared__ unsigned long long cubes_s;      // cubes this block visited (-> the device-counted sample total)
+  __shared__ unsigned int overflow_s;         // addends that overflowed to inf (words[-3])
   // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
-  const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (R == RngKind::philox ? 1u : 0u);
+  const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (philox_stream(R) ? 1u : 0u);
   double2* LW = reinterpret_cast<double2*>(smem);
   double* rcp = reinterpret_cast<double*>(LW + D * nb);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
@@ -366,7 +368,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     const int nwords = nacc * kXWords;
     for (int i = tid; i < nwords; i += nt) acc[i] = 0u;
     for (int i = tid; i < kRcpSmem; i += nt) rcp[i] = i ? 1.0 / static_cast<double>(i) : 0.0;
-    if (tid == 0) nonfinite_s = 0u;
+    if (tid == 0) {
+      nonfinite_s = 0u;
+      overflow_s = 0u;
+      cubes_s = 0ull;
+    }
     pdl_wait();  // the grid, the stop flag and the exchange words come from the previous kernels
     if (a.stop && *a.stop) return;  // (uniform across the block)
     if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
@@ -392,31 +398,41 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   // deposit word-major across the axes
   // (compat: the exact (f J)^2, as the reference's ExactBins; philox: rounded
   // to 24 significant bits -- one or two word atomics instead of three, exact.cuh)
+  constexpr bool kR24 = R == RngKind::philox;  // 24-bit bin addends (else exact, as ExactBins)
   auto deposit = [&](double fj, const std::uint32_t (&bin)[D]) {
-    using Dg = std::conditional_t<R == RngKind::compat, exact::Digits, exact::Digits2>;
+    using Dg = std::conditional_t<kR24, exact::Digits2, exact::Digits>;
     Dg dgt;
     bool nz;
-    if constexpr (R == RngKind::compat) nz = exact::split(__dmul_rn(fj, fj), dgt);
-    else nz = exact::split_r24(__dmul_rn(fj, fj), dgt);
+    const double sq = __dmul_rn(fj, fj);
+    // (f J)^2 overflowed (|f J| > ~1.3e154; with 24-bit addends also a value
+    // that RN24 rounds up to 2^1024): the reference's ExactSum::add throws
+    // (exact_sum.hpp:34) -- count it, the finish kernel stops the run
+    if (!(sq < (kR24 ? exact::kR24Max : INFINITY))) {
+      atomicAdd(&overflow_s, 1u);
+      return;
+    }
+    if constexpr (kR24) nz = exact::split_r24(sq, dgt);
+    else nz = exact::split(sq, dgt);
     if (nz) {
       const std::uint32_t wb = bins_s + 4u * dgt.w;
       if (bin_axes == static_cast<std::uint32_t>(D)) {
-        if constexpr (R == RngKind::philox && NB != 0) {  // row offsets as immediates
+        if constexpr (philox_stream(R) && NB != 0) {  // row offsets as immediates
           std::uint32_t base[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) base[j] = wb + bin[j] * kCell;
-          exact::add_digits2_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
+          if constexpr (kR24) exact::add_digits2_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
+          else exact::add_digits_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
         } else {
           std::uint32_t ad[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
-          if constexpr (R == RngKind::compat) exact::add_digits_s<D>(ad, end_s, dgt);
-          else exact::add_digits2_s<D>(ad, end_s, dgt);
+          if constexpr (kR24) exact::add_digits2_s<D>(ad, end_s, dgt);
+          else exact::add_digits_s<D>(ad, end_s, dgt);
         }
       } else {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
-        if constexpr (R == RngKind::compat) exact::add_digits_s<1>(ad, end_s, dgt);
-        else exact::add_digits2_s<1>(ad, end_s, dgt);
+        if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
+        else exact::add_digits_s<1>(ad, end_s, dgt);
       }
     }
   };
@@ -433,8 +449,10 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   for (int j = 0; j < D; ++j) coord(j);
 
   const std::uint32_t p = static_cast<std::uint32_t>(a.p);
+  std::uint32_t ncubes = 0;  // cubes this thread visited (counted, not derived: the coverage check)
   while (active) {
     const std::uint64_t t = cw.t;
+    ++ncubes;
     double sum, var;
     if constexpr (R == RngKind::compat) {
       const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
@@ -488,7 +506,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       sum = __dmul_rn(sum, a.scale);
       var = __dmul_rn(m2, a.rcp_pp1);
     }
-    if (!(var > 0.0)) var = 0.0;
+    if (!(var > 0.0)) var = 0.0;  // sampler.hpp:179 (a NaN variance becomes 0, an infinite one stays)
+    if (!(fabs(sum) < INFINITY) || !(var < INFINITY)) {  // ExactSum::add would throw (exact_sum.hpp:34)
+      atomicAdd(&overflow_s, 1u);
+      sum = var = 0.0;
+    }
     exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
 
     bool all_axes;
@@ -501,6 +523,12 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     }
   }
   MCB_K1_STAMP(3, atomicMin)
+  {  // the block's visited-cube count (warp sums in u64: a thread's count fits u32, a block's may not)
+    unsigned long long c = ncubes;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((tid & 31) == 0 && c) atomicAdd(&cubes_s, c);
+  }
   __syncthreads();
   MCB_K1_STAMP(4, atomicMax)
 
@@ -565,6 +593,10 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       if (sum) add_word(i, sum);
     }
     if (tid == 0 && nonfinite_s) add_word(-1, nonfinite_s);  // words[-1]: the non-finite count (own CTA's)
+    if (tid == 0 && overflow_s) add_word(-3, overflow_s);    // words[-3]: overflowed addends (own CTA's)
+    // words[-2]: finite samples taken = visited cubes * p - non-finite samples (own CTA's); the
+    // finish kernel turns it into the write count (samples * bin_axes, sampler.hpp:116-119)
+    if (tid == 0 && cubes_s) add_word(-2, cubes_s * a.p - nonfinite_s);
     if (csize == 2) cluster.sync();  // the partner has finished reading this CTA's accumulators
   }
   if (npeers) {

@@ -22,6 +22,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 XWORDS = 67  # words per exact accumulator (mcubes_oracle.c XW == MCB_XWORDS)
+# sample stream codes (include/mcubes_b200.h mcb_rng; orc_set_rng)
+RNG_CODES = {"compat": 0, "philox": 1, "philox_exact": 2}
 
 _D = C.c_double
 _U32 = C.c_uint32
@@ -73,6 +75,8 @@ def orc():
                                       _I, _PD, _PD, _PD, _PU64, _PD, _PD, _U32, _PD, _PU64, _PD, _PD]
         lib.orc_set_rng.argtypes = [_I]
         lib.orc_set_rng.restype = None
+        lib.orc_set_threads.argtypes = [_I]
+        lib.orc_set_threads.restype = None
         lib.orc_xwords.restype = _U32
         assert lib.orc_xwords() == XWORDS
         _orc = lib
@@ -176,13 +180,15 @@ def v_sample(lib_kind, integrand, params, d, nb, lower, upper, edges, m, s, p, s
             ep = ptr(e)
         bin_mode = 1 if mode in ("axis0", "serial_axis0") else 0
         kbins = 0 if mode == "frozen" else 1
-        lib.orc_set_rng(1 if rng == "philox" else 0)
+        lib.orc_set_rng(RNG_CODES[rng])
+        lib.orc_set_threads(threads if threads else 1)
         try:
             rc = lib.orc_v_sample(integrand, ptr(params), len(params), d, nb, lo, hi, ep, m, s, p, seed,
                                   iteration, bin_mode, kbins, C.byref(est), C.byref(var), ptr(contrib),
                                   C.byref(writes), ptr(ex), C.byref(efx))
         finally:
             lib.orc_set_rng(0)
+            lib.orc_set_threads(1)
         err = lib.orc_last_error
     if rc != 0:
         raise OracleError(rc, err().decode(), ex[:d].copy(), efx.value)
@@ -211,7 +217,7 @@ def integrate(lib_kind, integrand, params, d, nb, maxcalls, itmax, ita, tau, alp
         err = lib.ref_last_error
     else:
         lib = orc()
-        lib.orc_set_rng(1 if rng == "philox" else 0)
+        lib.orc_set_rng(RNG_CODES[rng])
         try:
             rc = lib.orc_integrate(integrand, ptr(params), len(params), d, nb, maxcalls, itmax, ita, tau,
                                    alpha, chi2max, seed, variant, darr(lower), darr(upper), ptr(res), sp,
@@ -229,3 +235,33 @@ def integrate(lib_kind, integrand, params, d, nb, maxcalls, itmax, ita, tau, alp
     if want_grids:
         out["grids"] = grids.reshape(itmax, d * nb)[:n].copy()
     return out
+
+
+def grid_adjust(lib_kind, d, nb, lower, upper, edges, contrib, alpha=1.5, symmetric=False):
+    """Grid::adjusted / adjusted_symmetric (grid.hpp:104-146) through the
+    oracle ('orc') or the compiled reference ('ref'); returns the new edges."""
+    np = _np()
+    out = np.zeros(d * nb)
+    e = np.ascontiguousarray(edges, dtype=np.float64)
+    c = np.ascontiguousarray(contrib, dtype=np.float64)
+    if lib_kind == "ref":
+        lib, err = ref(), ref().ref_last_error
+        rc = lib.ref_grid_adjust(d, nb, darr(lower), darr(upper), ptr(e), ptr(c), alpha, int(symmetric), ptr(out))
+    else:
+        lib, err = orc(), orc().orc_last_error
+        rc = lib.orc_grid_adjust(d, nb, darr(lower), darr(upper), ptr(e), ptr(c), alpha, int(symmetric), ptr(out))
+    if rc != 0:
+        raise OracleError(rc, err().decode())
+    return out
+
+
+def weighted_estimate(est, var):
+    """The reference's weighted_estimate (driver.hpp:146-169): (I, sigma, chi2/dof)."""
+    np = _np()
+    e = np.ascontiguousarray(est, dtype=np.float64)
+    v = np.ascontiguousarray(var, dtype=np.float64)
+    out = np.zeros(3)
+    rc = ref().ref_weighted_estimate(len(e), ptr(e), ptr(v), ptr(out))
+    if rc != 0:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    return float(out[0]), float(out[1]), float(out[2])

@@ -19,6 +19,7 @@
  * exact integer, so RN() of it is the same double.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -402,6 +403,14 @@ typedef struct {
   double bad_x[64];
 } partial;
 
+/* Host threads of orc_sample_partial (1 = the serial loop).  Threads take
+ * contiguous cube ranges and their exact partials are merged word-wise, so
+ * the result is the same for any thread count (the reference's own
+ * invariance, sampler.hpp:213-278); the first non-finite sample in cube order
+ * is the lowest range's. */
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
 /* run_cube (sampler.hpp:147-181), accumulating straight into exact words */
 static void run_cube(const orc_fn* f, const orc_grid* g, uint64_t t, uint64_t gi, uint64_t p,
                      uint64_t iter_root, double scale, uint32_t bin_axes, int kbins, partial* acc) {
@@ -447,6 +456,9 @@ static void run_cube(const orc_fn* f, const orc_grid* g, uint64_t t, uint64_t gi
   xacc_add_mag(sum_scaled < 0 ? &acc->est_neg : &acc->est_pos, sum_scaled);
   xacc_add_mag(&acc->var, var);
 }
+
+static int g_rng = 0; /* 0 = the reference stream, 1 = the Philox path twin (r24 bins), 2 = Philox, exact bins */
+void orc_set_rng(int rng) { g_rng = rng; }
 
 /* ---------------- Philox path twin (NOT the reference) ----------------
  * The B200 north-star stream (include/mcubes_b200/sampler.cuh,
@@ -518,12 +530,15 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
     const uint64_t nk = k + 1;
     mean = fma(dd, 1.0 / (double)nk, mean);
     m2 = fma(dd, fj - mean, m2);
-    if (kbins) { /* (f J)^2 rounded half-up to 24 significant bits (exact.cuh split_r24) */
+    if (kbins) { /* (f J)^2, rounded half-up to 24 significant bits on the r24 path (exact.cuh
+                  * split_r24; orc_set_rng(1)), exact with orc_set_rng(2) (philox_exact) */
       double sq = fj * fj;
-      uint64_t b;
-      memcpy(&b, &sq, 8);
-      b = (b + (1ull << 28)) & ~((1ull << 29) - 1);
-      memcpy(&sq, &b, 8);
+      if (g_rng == 1) {
+        uint64_t b;
+        memcpy(&b, &sq, 8);
+        b = (b + (1ull << 28)) & ~((1ull << 29) - 1);
+        memcpy(&sq, &b, 8);
+      }
       for (uint32_t j = 0; j < bin_axes; ++j) xacc_add_mag(&acc->bins[(size_t)j * nb + bin[j]], sq);
       acc->writes += bin_axes;
     }
@@ -535,8 +550,27 @@ static void run_cube_philox(const orc_fn* f, const orc_grid* g, uint64_t t, uint
   xacc_add_mag(&acc->var, var);
 }
 
-static int g_rng = 0; /* 0 = the reference stream, 1 = the Philox path twin */
-void orc_set_rng(int rng) { g_rng = rng; }
+
+/* one thread's contiguous cube range [t0, t1) (sample_all_cubes' batches) */
+typedef struct {
+  const orc_fn* f;
+  const orc_grid* g;
+  uint64_t gi, p, root, t0, t1;
+  double scale;
+  uint32_t bin_axes;
+  int kbins;
+  partial acc;
+} range_job;
+
+static void* range_worker(void* arg) {
+  range_job* jb = (range_job*)arg;
+  for (uint64_t t = jb->t0; t < jb->t1; ++t) {
+    if (g_rng) run_cube_philox(jb->f, jb->g, t, jb->gi, jb->p, jb->root, jb->scale, jb->bin_axes, jb->kbins, &jb->acc);
+    else run_cube(jb->f, jb->g, t, jb->gi, jb->p, jb->root, jb->scale, jb->bin_axes, jb->kbins, &jb->acc);
+    if (jb->acc.bad) break;
+  }
+  return NULL;
+}
 
 /* Exact partial over cubes [c0, c1) in the GPU exchange format: out_words
  * receives (3 + bin_axes*nb) accumulators of XW words:
@@ -558,15 +592,57 @@ int orc_sample_partial(int id, const double* params, uint32_t nparams, uint32_t 
   const double scale = 1.0 / ((double)m * (double)p);
   const uint32_t bin_axes = bin_mode == 0 ? d : 1;
   orc_grid g = {d, nb, lower, upper, edges};
+  const uint64_t iter_root = orc_iteration_root(seed, iteration);
+  if (c1 > m) c1 = m;
+  if (c0 > c1) c0 = c1;
+  const uint64_t span = c1 - c0;
+  int nth = g_threads;
+  if ((uint64_t)nth > span / 64 + 1) nth = (int)(span / 64 + 1);
+  range_job* jobs = calloc((size_t)nth, sizeof(range_job));
+  pthread_t* tids = calloc((size_t)nth, sizeof(pthread_t));
+  for (int i = 0; i < nth; ++i) {
+    range_job* jb = &jobs[i];
+    jb->f = &f;
+    jb->g = &g;
+    jb->gi = gi;
+    jb->p = p;
+    jb->root = iter_root;
+    jb->scale = scale;
+    jb->bin_axes = bin_axes;
+    jb->kbins = kbins;
+    jb->t0 = c0 + span * (uint64_t)i / (uint64_t)nth;
+    jb->t1 = c0 + span * (uint64_t)(i + 1) / (uint64_t)nth;
+    jb->acc.bins = calloc((size_t)bin_axes * nb, sizeof(xacc));
+    if (nth > 1) pthread_create(&tids[i], NULL, range_worker, jb);
+    else range_worker(jb);
+  }
   partial acc;
   memset(&acc, 0, sizeof acc);
-  acc.bins = calloc((size_t)bin_axes * nb, sizeof(xacc));
-  const uint64_t iter_root = orc_iteration_root(seed, iteration);
-  for (uint64_t t = c0; t < c1 && t < m; ++t) {
-    if (g_rng) run_cube_philox(&f, &g, t, gi, p, iter_root, scale, bin_axes, kbins, &acc);
-    else run_cube(&f, &g, t, gi, p, iter_root, scale, bin_axes, kbins, &acc);
-    if (acc.bad) break;
+  acc.bins = jobs[0].acc.bins;
+  for (int i = 0; i < nth; ++i) {
+    if (nth > 1) pthread_join(tids[i], NULL);
+    partial* q = &jobs[i].acc;
+    if (q->bad && !acc.bad) {
+      acc.bad = 1;
+      acc.bad_fx = q->bad_fx;
+      memcpy(acc.bad_x, q->bad_x, sizeof acc.bad_x);
+    }
+    if (i == 0) {
+      acc.est_pos = q->est_pos;
+      acc.est_neg = q->est_neg;
+      acc.var = q->var;
+      acc.writes = q->writes;
+      continue;
+    }
+    xacc_merge(&acc.est_pos, &q->est_pos);
+    xacc_merge(&acc.est_neg, &q->est_neg);
+    xacc_merge(&acc.var, &q->var);
+    for (size_t c = 0; c < (size_t)bin_axes * nb; ++c) xacc_merge(&acc.bins[c], &q->bins[c]);
+    acc.writes += q->writes;
+    free(q->bins);
   }
+  free(jobs);
+  free(tids);
   if (acc.bad) {
     if (err_x) memcpy(err_x, acc.bad_x, sizeof(double) * d);
     if (err_fx) *err_fx = acc.bad_fx;

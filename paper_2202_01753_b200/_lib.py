@@ -71,6 +71,8 @@ SIGNATURES = {
                                          _U64, _U64, _U64, _U64, _U64, _PD, _PD]),
     "mcb_v_sample_philox": (C.c_int, [_VP, C.POINTER(mcb_integrand), _U32, _U32, _PD, _PD, _PD, _U64,
                                       _U64, _U64, _U64, _U64, _I32, _PD, _PD, _PD, _PU64]),
+    "mcb_v_sample_rng": (C.c_int, [_VP, C.POINTER(mcb_integrand), _I32, _U32, _U32, _PD, _PD, _PD, _U64,
+                                   _U64, _U64, _U64, _U64, _I32, _PD, _PD, _PD, _PU64]),
     "mcb_grid_adjust": (C.c_int, [_VP, _U32, _U32, _PD, _PD, _PD, _PD, _D, _I32, _PD]),
     "mcb_setup": (C.c_int, [C.POINTER(mcb_config), _PU64, _PU64, _PU64, _PU64]),
     "mcb_set_batch_size": (C.c_int, [_U64, _U32, _PU64]),

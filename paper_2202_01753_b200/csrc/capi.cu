@@ -121,7 +121,9 @@ mcubes::RunConfig to_cfg(const mcb_config* c) {
   if (c->lower) cfg.lower.assign(c->lower, c->lower + c->dims);
   if (c->upper) cfg.upper.assign(c->upper, c->upper + c->dims);
   cfg.workers = c->workers;
-  cfg.rng = c->rng == MCB_RNG_PHILOX ? RngKind::philox : RngKind::compat;
+  if (c->rng != MCB_RNG_COMPAT && c->rng != MCB_RNG_PHILOX && c->rng != MCB_RNG_PHILOX_EXACT)
+    throw std::invalid_argument("RunConfig: unknown rng " + std::to_string(c->rng));
+  cfg.rng = static_cast<RngKind>(c->rng);
   return cfg;
 }
 
@@ -160,7 +162,7 @@ int v_sample_impl(mcb_ctx* c, const mcb_integrand* f, uint32_t dims, uint32_t n_
     if (est) *est = r.est;
     if (var) *var = r.var;
     if (contrib && bin_axes) std::memcpy(contrib, r.contrib.data(), sizeof(double) * r.contrib.size());
-    if (writes) *writes = m * p * bin_axes;
+    if (writes) *writes = r.writes;  // device-counted deposits (sampler.hpp:116-119)
   });
 }
 
@@ -224,6 +226,20 @@ int mcb_v_sample_philox(mcb_ctx* c, const mcb_integrand* f, uint32_t dims, uint3
                        : bin_update == MCB_BIN_AXIS0_ONLY ? MCB_BIN_AXIS0_ONLY : MCB_BIN_ALL_AXES;
   return v_sample_impl(c, f, dims, n_bins, lower, upper, edges, m, s, p, seed, iteration, mode, RngKind::philox,
                        est, var, mode < 0 ? nullptr : contrib, mode < 0 ? nullptr : writes);
+}
+
+int mcb_v_sample_rng(mcb_ctx* c, const mcb_integrand* f, int32_t rng, uint32_t dims, uint32_t n_bins,
+                     const double* lower, const double* upper, const double* edges, uint64_t m, uint64_t s,
+                     uint64_t p, uint64_t seed, uint64_t iteration, int32_t bin_update, double* est, double* var,
+                     double* contrib, uint64_t* writes) {
+  if (rng != MCB_RNG_COMPAT && rng != MCB_RNG_PHILOX && rng != MCB_RNG_PHILOX_EXACT) {
+    if (c) c->err = "unknown rng " + std::to_string(rng);
+    return MCB_EINVAL;
+  }
+  const int32_t mode = bin_update == MCB_BIN_NONE ? -1
+                       : bin_update == MCB_BIN_AXIS0_ONLY ? MCB_BIN_AXIS0_ONLY : MCB_BIN_ALL_AXES;
+  return v_sample_impl(c, f, dims, n_bins, lower, upper, edges, m, s, p, seed, iteration, mode,
+                       static_cast<RngKind>(rng), est, var, mode < 0 ? nullptr : contrib, mode < 0 ? nullptr : writes);
 }
 
 int mcb_v_sample_no_adjust(mcb_ctx* c, const mcb_integrand* f, uint32_t dims, uint32_t n_bins,

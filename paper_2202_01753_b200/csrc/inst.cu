@@ -11,7 +11,11 @@ namespace mcubes::gpu::abi {
 
 template <class F>
 static IntegrandOps both(RngKind rng, const F& f) {
-  return rng == RngKind::philox ? make_ops<F, RngKind::philox>(f) : make_ops<F, RngKind::compat>(f);
+  switch (rng) {
+    case RngKind::philox: return make_ops<F, RngKind::philox>(f);
+    case RngKind::philox_exact: return make_ops<F, RngKind::philox_exact>(f);
+    default: return make_ops<F, RngKind::compat>(f);
+  }
 }
 
 #if MCB_INST == 0

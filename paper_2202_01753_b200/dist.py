@@ -156,54 +156,54 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
     events = [torch.cuda.Event() for _ in range(ahead + 1)]
     with torch.cuda.stream(stream):
         run = M.Run(f, cfg, ctx)
-        run.set_progress(flags.data_ptr())
-        n0, n1 = partition(run.work_items, world, rank)
         peers = None
-        if transport == "peer":
-            torch.cuda.current_stream(dev).synchronize()
-            peers = PeerExchange(ctx, run.exchange_words(), group)
-            peers.attach(run)
-        else:
-            xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
-            run.set_exchange(xbuf.data_ptr())
-        first = run.resume(resume) if resume is not None else 1
-        if first > 1 and run.result().converged:
-            res = run.result()
-            run.close()
-            if peers is not None:
-                peers.close()
-            return res
-        for it in range(first, cfg.itmax + 1):
-            if observer is None and it >= first + ahead:
-                events[(it - ahead) % (ahead + 1)].synchronize()
-                if int(flags[it - ahead - 1]) != 1:
-                    break
-            run.sample(it, n0, n1)
-            run.reduce(it)
-            if peers is None:
-                # exact integer sum across ranks, of the words this iteration uses
-                # (frozen iterations: the count word and est+/est-/var only)
-                dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
-            run.finish(it)
-            events[it % (ahead + 1)].record(stream)
-            if observer is not None:
-                r = run.result()
-                if r.iterations_used < it:
-                    break
-                observer(it, r, run.grid())
-        # A non-finite sample in any rank's slice stops every rank at the same
-        # iteration (its count is exchanged with the words); report the first
-        # one in serial order over all slices, as a single process would.
-        failed, key = run.failure_key()
-        if failed:
-            k = torch.tensor([key - (1 << 63)], dtype=torch.int64, device=dev)  # u64 order in int64
-            dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
-            run.set_failure_key(int(k.item()) + (1 << 63))
         try:
-            res = run.result()
+            run.set_progress(flags.data_ptr())
+            n0, n1 = partition(run.work_items, world, rank)
+            if transport == "peer":
+                torch.cuda.current_stream(dev).synchronize()
+                peers = PeerExchange(ctx, run.exchange_words(), group)
+                peers.attach(run)
+            else:
+                xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
+                run.set_exchange(xbuf.data_ptr())
+            first = run.resume(resume) if resume is not None else 1
+            if first > 1 and run.result().converged:
+                return run.result()
+            for it in range(first, cfg.itmax + 1):
+                if observer is None and it >= first + ahead:
+                    events[(it - ahead) % (ahead + 1)].synchronize()
+                    if int(flags[it - ahead - 1]) != 1:
+                        break
+                run.sample(it, n0, n1)
+                run.reduce(it)
+                if peers is None:
+                    # exact integer sum across ranks, of the words this iteration uses
+                    # (frozen iterations: the count words and est+/est-/var only)
+                    dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
+                run.finish(it)
+                events[it % (ahead + 1)].record(stream)
+                if observer is not None:
+                    # a failed iteration stops here, before result() (which raises): the
+                    # failure key is min-reduced over the ranks below first, as the C++
+                    # loop does (`if (st.failed) break`)
+                    if run.failure_key()[0]:
+                        break
+                    r = run.result()
+                    if r.iterations_used < it:
+                        break
+                    observer(it, r, run.grid())
+            # A non-finite sample in any rank's slice stops every rank at the same
+            # iteration (its count is exchanged with the words); report the first
+            # one in serial order over all slices, as a single process would.
+            failed, key = run.failure_key()
+            if failed:
+                k = torch.tensor([key - (1 << 63)], dtype=torch.int64, device=dev)  # u64 order in int64
+                dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
+                run.set_failure_key(int(k.item()) + (1 << 63))
+            return run.result()
         finally:
             run.close()
             if peers is not None:
                 torch.cuda.current_stream(dev).synchronize()
                 peers.close()
-    return res

@@ -518,20 +518,38 @@ class EstimateVariance:
     raw_variance: float
 
 
+RNG_CODES = {"compat": 0, "philox": 1, "philox_exact": 2}  # include/mcubes_b200.h mcb_rng
+
+
+def rng_code(rng: str, bins: str = "") -> int:
+    """mcb_rng for a (stream, bin precision) pair.  bins '' = the stream's
+    default: exact for compat (the reference's ExactBins), r24 for philox
+    ((f J)^2 rounded to 24 significant bits, then summed exactly)."""
+    if rng == "compat":
+        if bins not in ("", "exact"):
+            raise ValueError("the compat stream sums exact bins (it is bitwise the reference)")
+        return 0
+    if rng == "philox":
+        if bins not in ("", "r24", "exact"):
+            raise ValueError("bins must be 'r24' or 'exact'")
+        return 2 if bins == "exact" else 1
+    raise ValueError(f"unknown rng {rng!r}: 'compat' or 'philox'")
+
+
 def v_sample(f: IntegrandSpec, grid: Grid, m: int, s: int, p: int, seed: int, iteration: int,
              mode: BinUpdate = BinUpdate.all_axes, max_threads: int = 0, rng: str = "compat",
-             ctx: Optional[Context] = None) -> SampleOutcome:
+             ctx: Optional[Context] = None, bins: str = "") -> SampleOutcome:
     """One adjusting iteration on the GPU (sampler.hpp:312-333).  Output is
-    bitwise identical for any ``s``/``max_threads`` (accepted, as in the reference)."""
+    bitwise identical for any ``s``/``max_threads`` (accepted, as in the
+    reference).  ``writes()`` of the result is counted on the device."""
     ctx = ctx or default_context()
-    lib = L.lib()
     fs, keep = f._c()
     lo, hi = _f64(grid.lowers), _f64(grid.uppers)
     est, var, writes = C.c_double(), C.c_double(), C.c_uint64()
     contrib = np.zeros(grid.dims() * grid.n_bins())
-    fn = lib.mcb_v_sample_philox if rng == "philox" else lib.mcb_v_sample
-    rc = fn(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo), _dptr(hi), _dptr(grid.raw_edges),
-            m, s, p, seed, iteration, int(mode), C.byref(est), C.byref(var), _dptr(contrib), C.byref(writes))
+    rc = L.lib().mcb_v_sample_rng(ctx.ptr, C.byref(fs), rng_code(rng, bins), grid.dims(), grid.n_bins(), _dptr(lo),
+                                  _dptr(hi), _dptr(grid.raw_edges), m, s, p, seed, iteration, int(mode),
+                                  C.byref(est), C.byref(var), _dptr(contrib), C.byref(writes))
     _raise(rc, ctx.ptr, grid.dims())
     return SampleOutcome(est.value, var.value, BinAccumulator(grid.dims(), grid.n_bins(), contrib, writes.value))
 
@@ -544,9 +562,9 @@ def v_sample_no_adjust(f: IntegrandSpec, grid: Grid, m: int, s: int, p: int, see
     lo, hi = _f64(grid.lowers), _f64(grid.uppers)
     est, var = C.c_double(), C.c_double()
     if rng == "philox":
-        rc = L.lib().mcb_v_sample_philox(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo), _dptr(hi),
-                                         _dptr(grid.raw_edges), m, s, p, seed, iteration, 2, C.byref(est),
-                                         C.byref(var), None, None)
+        rc = L.lib().mcb_v_sample_rng(ctx.ptr, C.byref(fs), 1, grid.dims(), grid.n_bins(), _dptr(lo), _dptr(hi),
+                                      _dptr(grid.raw_edges), m, s, p, seed, iteration, 2, C.byref(est),
+                                      C.byref(var), None, None)
     else:
         rc = L.lib().mcb_v_sample_no_adjust(ctx.ptr, C.byref(fs), grid.dims(), grid.n_bins(), _dptr(lo),
                                             _dptr(hi), _dptr(grid.raw_edges), m, s, p, seed, iteration,
@@ -573,7 +591,10 @@ def parse_variant(s: str) -> Optional[Variant]:
 
 @dataclass
 class RunConfig:
-    """driver.hpp:37-71 (plus ``rng``: 'compat' = the reference stream, 'philox')."""
+    """driver.hpp:37-71, plus ``rng`` ('compat' = the reference stream, bitwise
+    the reference; 'philox' = the north-star stream) and ``bins`` (the
+    contribution precision: '' = the stream's default, 'exact' or 'r24'; see
+    rng_code)."""
 
     dims: int = 0
     n_bins: int = 50
@@ -589,13 +610,14 @@ class RunConfig:
     upper: List[float] = field(default_factory=list)
     workers: int = 0
     rng: str = "compat"
+    bins: str = ""
 
     def _c(self):
         lo, hi = _f64(self.lower), _f64(self.upper)
         c = L.mcb_config(self.dims, self.n_bins, self.maxcalls, self.itmax, self.ita, self.tau_rel, self.alpha,
                          self.chi2_dof_max, self.seed, int(self.variant), self.workers,
                          _dptr(lo) if lo.size else None, _dptr(hi) if hi.size else None,
-                         1 if self.rng == "philox" else 0, 0)
+                         rng_code(self.rng, self.bins), 0)
         return c, (lo, hi)
 
     def validate(self):

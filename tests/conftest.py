@@ -58,14 +58,15 @@ def ctx():
 
 def words_value(words) -> list:
     """Exact integers denoted by an exchange buffer ([accumulator][MCB_XWORDS]
-    radix-2^32 digit sums, after the leading non-finite count word of a run's
-    buffer).  Different partitions carry between words at different points,
-    so compare VALUES, not word vectors."""
+    radix-2^32 digit sums, after the MCB_XHEADER count words of a run's
+    buffer: overflowed addends, finite samples, non-finite samples).
+    Different partitions carry between words at different points, so compare
+    VALUES, not word vectors."""
     a = np.asarray(words).astype(np.uint64)
     out = []
-    if a.size % 67 == 1:  # a run's exchange buffer: [non-finite count][accumulators]
-        out.append(int(a[0]))
-        a = a[1:]
+    if a.size % 67 == 3:  # a run's exchange buffer: [3 count words][accumulators]
+        out += [int(v) for v in a[:3]]
+        a = a[3:]
     a = a.reshape(-1, 67)
     for row in a:
         v = 0

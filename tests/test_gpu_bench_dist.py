@@ -1,0 +1,56 @@
+"""GPU: bench.py's N > 1 path end to end -- torchrun with world 4, all ranks on
+cuda:0, the exchange all-reduced over gloo (MCB_DIST_BACKEND=gloo; NCCL on a
+real 8xB200 box).  The cube-range partition with an exact integer exchange
+must give the single-GPU run's estimate bit for bit, for both transports."""
+from __future__ import annotations
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+ARGS = ["--steps", "2", "--warmup", "3", "--maxcalls", str(10 ** 8), "--no-cpu", "--no-secondary"]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _line(out: str) -> dict:
+    return json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+
+
+def _bench(world, transport="collective"):
+    env = dict(os.environ, MCB_DIST_BACKEND="gloo")
+    if world == 1:
+        cmd = [sys.executable, "bench.py", *ARGS]
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", str(world),
+               "--transport", transport, *ARGS]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return _line(p.stdout)
+
+
+@pytest.mark.parametrize("transport", ["collective", "peer"])
+def test_bench_world4_matches_single_gpu(transport):
+    one = _bench(1)
+    four = _bench(4, transport)
+    assert four["n_gpus"] == 4 and one["n_gpus"] == 1
+    assert four["config"] == one["config"]
+    # exact exchange: identical estimate, sigma and device-counted samples
+    for k in ("estimate", "sigma", "chi2_dof", "samples", "bin_writes"):
+        assert four["result"][k] == one["result"][k], k
+    assert four["result"]["samples"] == (3 + 2) * one["config"]["evals_per_step"]

@@ -28,7 +28,7 @@ def test_abi_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
-    assert lib.mcb_abi_version() == 1
+    assert lib.mcb_abi_version() == 2
 
 
 def test_library_is_sm100a():

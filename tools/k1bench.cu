@@ -41,6 +41,8 @@ int main(int argc, char** argv) {
     const Grid g(D, 50, cfg.lower, cfg.upper);
     gpu::upload(ctx, ctx.edges, g.raw_edges().data(), D * 50);
     gpu::upload(ctx, ctx.lower, cfg.lower.data(), D);
+    ctx.grid_edges = ctx.edges.get();
+    ctx.grid_lower = ctx.lower.get();
     unsigned long long* err = ctx.err_key.ensure(1);
     MCB_CUDA(cudaMemsetAsync(err, 0xff, 8, ctx.stream()));
     const std::uint64_t key = direct_key == 0 ? gpu::iteration_key(cfg.seed, 1) : static_cast<std::uint64_t>(direct_key);
@@ -49,13 +51,13 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a1);
     float best = 1e30f;
     const int between = std::getenv("K1_BETWEEN") ? std::atoi(std::getenv("K1_BETWEEN")) : 0;
-    const std::size_t nwords = 1 + static_cast<std::size_t>(gpu::exchange_accs(D, 50)) * gpu::kXWords;
-    unsigned long long* words = ctx.words.ensure(nwords) + 1;  // [non-finite count][accumulators]
+    const std::size_t nwords = gpu::kXHeader + static_cast<std::size_t>(gpu::exchange_accs(D, 50)) * gpu::kXWords;
+    unsigned long long* words = ctx.words.ensure(nwords) + gpu::kXHeader;  // [counts][accumulators]
     for (int r = 0; r < reps + 1; ++r) {
       cudaEventRecord(a0, ctx.stream());
       (void)ops.k1(ctx, sh, frozen ? 0u : D, key, 0, sh.m, nullptr, err, words);
       cudaEventRecord(a1, ctx.stream());
-      if (between == 1) cudaMemsetAsync(words - 1, 0, sizeof(unsigned long long) * nwords, ctx.stream());
+      if (between == 1) cudaMemsetAsync(words - gpu::kXHeader, 0, sizeof(unsigned long long) * nwords, ctx.stream());
       cudaEventSynchronize(a1);
       if (between == 2) usleep(200000);
       float ms;
