@@ -658,6 +658,35 @@ def run_suite(path: str):
     out.close()
 
 
+def run_scale(args):
+    """bench_cli scale (GPU columns, at this launch's GPU count) with the
+    reference CPU adjusting iteration -- v_sample + Grid::adjusted through
+    oracle/_ref on all host threads -- timed beside each cell (rank 0)."""
+    import types
+
+    import oracle as O
+    from paper_2202_01753_b200 import bench_cli
+
+    threads = os.cpu_count() or 1
+
+    def cpu_timer(integrand, d, maxcalls):
+        if not O.ref_available() or integrand not in {f"f{i}" for i in range(1, 7)}:
+            return None
+        fam = int(integrand[1])
+        lo, hi = [0.0] * d, [1.0] * d
+        sp = (O._U64 * 4)()
+        assert O.ref().ref_setup(d, N_BINS, maxcalls, 3, 3, 1e-3, ALPHA, 1.5, O.darr(lo), O.darr(hi), threads, sp) == 0
+        edges = O.uniform_edges(d, N_BINS, lo, hi)
+        t0 = time.perf_counter()
+        r = O.v_sample("ref", fam, None, d, N_BINS, lo, hi, edges, sp[1], sp[3], sp[2], 0, 1, "all", threads)
+        O.grid_adjust("ref", d, N_BINS, lo, hi, edges, r["contrib"], ALPHA)
+        return threads, 1e3 * (time.perf_counter() - t0)
+
+    o = types.SimpleNamespace(integrand=args.scale_integrand, dims=args.scale_dims, ncalls=args.scale_ncalls,
+                              rng=args.rng, cpu_max_evals=args.scale_cpu_max_evals, out=args.scale)
+    return bench_cli.cmd_scale(o, cpu_timer)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -676,6 +705,13 @@ def main():
                          "peer memory (CUDA IPC over NVLink)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
     ap.add_argument("--suite", default=None, help="run BASELINE configs 1-5 (GPU + reference CPU) into this JSONL")
+    ap.add_argument("--scale", default=None,
+                    help="BASELINE config 5: bench_cli's scale sweep at this launch's GPU count (torchrun for N > 1) "
+                         "with the reference CPU iteration timed on the host cores beside each cell, CSV here")
+    ap.add_argument("--scale-dims", default="2,4,6,8,10")
+    ap.add_argument("--scale-ncalls", default="1e6,1e8,1e10")
+    ap.add_argument("--scale-integrand", default="f4")
+    ap.add_argument("--scale-cpu-max-evals", type=float, default=1e9)
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")
@@ -688,6 +724,8 @@ def main():
         return run_reference(args, rank)
     if args.suite:
         return run_suite(args.suite)
+    if args.scale:
+        return run_scale(args)
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -298,6 +298,7 @@ struct Launch {
   int blocks = 0;
   std::size_t smem = 0;
   std::uint32_t pnb = 0;  ///< histogram cells per axis (n_bins, +1 padding cell on the Philox path)
+  std::uint32_t passes = 1;  ///< bin passes (> 1 when the histograms exceed one CTA's shared memory)
 };
 
 /// Cells per axis in K1's shared histogram for a stream kind.
@@ -335,10 +336,26 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   constexpr int kThreads = sample_threads(R, D);
   Launch L;
   L.pnb = partial_bins(R, sh.nb);
-  L.smem = sample_smem_bytes(D, L.pnb, bin_axes);
-  if (L.smem > static_cast<std::size_t>(ctx.max_smem()))
-    throw std::invalid_argument("B200 path: dims*n_bins too large for the shared-memory histogram (" +
-                                std::to_string(L.smem) + " B > " + std::to_string(ctx.max_smem()) + " B)");
+  // Bin passes: when bin_axes x (n_bins + 1) exact accumulators do not fit one
+  // CTA's shared memory, the axes are split over passes that re-sample the
+  // same keyed points (SampleArgs::bin_lo/bin_n); results are bitwise those of
+  // one pass.
+  const auto fits = [&](std::uint32_t na) {
+    return sample_smem_bytes(D, L.pnb, na) <= static_cast<std::size_t>(ctx.max_smem());
+  };
+  std::uint32_t passes = 1, per_pass = bin_axes;
+  if (!fits(bin_axes)) {
+    std::uint32_t most = bin_axes;
+    while (most > 1 && !fits(most)) --most;
+    if (!fits(most))
+      throw std::invalid_argument("B200 path: n_bins too large for one axis' shared-memory histogram (" +
+                                  std::to_string(sample_smem_bytes(D, L.pnb, 1)) + " B > " +
+                                  std::to_string(ctx.max_smem()) + " B)");
+    passes = (bin_axes + most - 1) / most;
+    per_pass = (bin_axes + passes - 1) / passes;  // balanced
+  }
+  L.passes = passes;
+  L.smem = sample_smem_bytes(D, L.pnb, per_pass);
   // attribute + occupancy queries are cached per instantiation (host latency
   // matters for small-ncall iterations)
   thread_local std::size_t cached_smem = 0;
@@ -431,8 +448,15 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   // reductions per SM.  Two-CTA clusters keep all 148 SMs usable at one CTA
   // per SM (tools/microbench/clusters.cu).
   const unsigned cluster = (L.blocks % 2 == 0 && k1_cluster_enabled()) ? 2u : 1u;
-  launch_pdl_cluster(kern, L.blocks, threads, L.smem, ctx.stream(), cluster, a, f);
-  ++ctx.launches;
+  for (std::uint32_t q = 0; q < passes; ++q) {
+    a.bin_lo = q * per_pass;
+    a.bin_n = std::min(per_pass, bin_axes - a.bin_lo);
+    a.scalars = q == 0 ? 1u : 0u;
+    a.publish = q + 1 == passes ? 1u : 0u;
+    const std::size_t smem = sample_smem_bytes(D, L.pnb, a.bin_n);
+    launch_pdl_cluster(kern, L.blocks, threads, smem, ctx.stream(), cluster, a, f);
+    ++ctx.launches;
+  }
   return L;
 }
 
@@ -465,7 +489,7 @@ void launch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t iter_
 /// Compile-time dimension dispatch.  The set of instantiated dimensions can
 /// be narrowed with MCB_DIMS_MAX to trade compile time for coverage.
 #ifndef MCB_DIMS_MAX
-#define MCB_DIMS_MAX 16
+#define MCB_DIMS_MAX 20
 #endif
 
 template <class F, RngKind R>
@@ -476,13 +500,14 @@ Launch dispatch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_
 #define MCB_CASE(D) \
   case D:           \
     if constexpr (D <= MCB_DIMS_MAX) {                                                                                  \
-      if (sh.nb == 50)                                                                                                \
-        return launch_k1<F, D, R, 50>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);               \
+      if (sh.nb == 50 && D <= 16) /* the compile-time n_bins fast path up to 16 axes */                              \
+        return launch_k1<F, D, R, (D <= 16 ? 50 : 0)>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words); \
       return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);                  \
     }                                                                                                                   \
     break;
     MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
-    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16)
+    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16) \
+    MCB_CASE(17) MCB_CASE(18) MCB_CASE(19) MCB_CASE(20)
 #undef MCB_CASE
     default:
       break;
@@ -499,7 +524,8 @@ void dispatch_point(Context& ctx, const F& f, const Shape& sh, std::uint64_t ite
     if constexpr (D <= MCB_DIMS_MAX) { launch_point<F, D, R>(ctx, f, sh, iter_root, t, k, out_x, out_fx); return; } \
     break;
     MCB_CASE(1) MCB_CASE(2) MCB_CASE(3) MCB_CASE(4) MCB_CASE(5) MCB_CASE(6) MCB_CASE(7) MCB_CASE(8)
-    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16)
+    MCB_CASE(9) MCB_CASE(10) MCB_CASE(11) MCB_CASE(12) MCB_CASE(13) MCB_CASE(14) MCB_CASE(15) MCB_CASE(16) \
+    MCB_CASE(17) MCB_CASE(18) MCB_CASE(19) MCB_CASE(20)
 #undef MCB_CASE
     default:
       break;

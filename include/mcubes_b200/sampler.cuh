@@ -51,7 +51,15 @@ struct SampleArgs {
   const double* lower;  ///< device, dims
   std::uint32_t dims, nb;
   std::uint32_t bin_axes;  ///< 0 = frozen (v_sample_no_adjust), 1 = axis0_only, dims = all_axes
-  std::uint32_t pad0;
+  /// Axes [bin_lo, bin_lo + bin_n) deposit bins in this launch.  A shape
+  /// whose bin_axes x (n_bins + 1) exact accumulators exceed one CTA's shared
+  /// memory is sampled in several passes over the same (keyed, hence
+  /// identical) points, each holding the histograms of a subset of the axes;
+  /// the first pass (`scalars`) also sums the estimate, the variance and the
+  /// sample counts.  Single pass: bin_lo = 0, bin_n = bin_axes, scalars = 1.
+  std::uint32_t bin_lo, bin_n;
+  std::uint32_t scalars;
+  std::uint32_t publish;  ///< peer exchange: this (last) pass publishes the iteration flag
   std::uint64_t m, p, g;
   double nbd;      ///< double(nb)
   double gd;       ///< double(g)
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   double2* LW = reinterpret_cast<double2*>(smem);
   double* rcp = reinterpret_cast<double*>(LW + D * nb);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
-  const int nacc = block_accs(a.bin_axes, nb);
+  const int nacc = block_accs(a.bin_n, nb);
   const int tid = threadIdx.x, nt = blockDim.x;
 
   {  // zero the accumulators, stage the grid and the Welford reciprocals
@@ -391,7 +399,8 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   const std::uint32_t var_s = acc_s + (2 * kLaneCopies + lane) * kAccBytes;
   const std::uint32_t bins_s = acc_s + kScalarAccs * kLaneCopies * kAccBytes;
   const std::uint32_t end_s = acc_s + static_cast<std::uint32_t>(nacc) * kAccBytes;
-  const std::uint32_t bin_axes = a.bin_axes;
+  const std::uint32_t bin_n = a.bin_n, bin_lo = a.bin_lo;
+  const bool scalars = a.scalars != 0;
   constexpr std::uint32_t kCell = 4u * kXWords;  // bytes per accumulator
 
   // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once,
@@ -415,7 +424,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     else nz = exact::split(sq, dgt);
     if (nz) {
       const std::uint32_t wb = bins_s + 4u * dgt.w;
-      if (bin_axes == static_cast<std::uint32_t>(D)) {
+      if (bin_n == static_cast<std::uint32_t>(D)) {  // every axis in one pass (the common case)
         if constexpr (philox_stream(R) && NB != 0) {  // row offsets as immediates
           std::uint32_t base[D];
 #pragma unroll
@@ -429,10 +438,20 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
           if constexpr (kR24) exact::add_digits2_s<D>(ad, end_s, dgt);
           else exact::add_digits_s<D>(ad, end_s, dgt);
         }
-      } else {  // BinUpdate::axis0_only
+      } else if (bin_n == 1 && bin_lo == 0) {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
         if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
         else exact::add_digits_s<1>(ad, end_s, dgt);
+      } else {  // a pass over axes [bin_lo, bin_lo + bin_n) (compile-time axis index, runtime predicate)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const std::uint32_t rel = static_cast<std::uint32_t>(j) - bin_lo;
+          if (rel < bin_n) {
+            const std::uint32_t ad[1] = {wb + bin[j] * kCell + rel * nb * kCell};
+            if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
+            else exact::add_digits_s<1>(ad, end_s, dgt);
+          }
+        }
       }
     }
   };
@@ -452,7 +471,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   std::uint32_t ncubes = 0;  // cubes this thread visited (counted, not derived: the coverage check)
   while (active) {
     const std::uint64_t t = cw.t;
-    ++ncubes;
+    ncubes += scalars ? 1u : 0u;
     double sum, var;
     if constexpr (R == RngKind::compat) {
       const std::uint64_t croot = rng::feed(a.iter_root, t);  // rng.hpp:51-54
@@ -465,7 +484,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point<F, D, NB>(a, f, LW, cd, croot, k, x, bin, fx);
         if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-          atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
+          if (scalars) atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
           continue;
         }
         sum = __dadd_rn(sum, __dmul_rn(fj, a.scale));
@@ -476,7 +495,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
                                                                    : __ddiv_rn(dd, static_cast<double>(nk));
         mean = __dadd_rn(mean, q);
         m2 = __dadd_rn(m2, __dmul_rn(dd, __dsub_rn(fj, mean)));
-        if (bin_axes) deposit(fj, bin);
+        if (bin_n) deposit(fj, bin);
       }
       var = div_rn(m2, a.pp1, a.rcp_pp1);  // sampler.hpp:178-179
     } else {
@@ -491,7 +510,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double fj = sample_point_fast<F, D, NB>(a, f, LW, cw.dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
-          atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
+          if (scalars) atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
           continue;
         }
         sum = __dadd_rn(sum, fj);
@@ -501,17 +520,19 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         const double dd = __dsub_rn(fj, mean);
         mean = __fma_rn(dd, y, mean);
         m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
-        if (bin_axes) deposit(fj, bin);
+        if (bin_n) deposit(fj, bin);
       }
       sum = __dmul_rn(sum, a.scale);
       var = __dmul_rn(m2, a.rcp_pp1);
     }
     if (!(var > 0.0)) var = 0.0;  // sampler.hpp:179 (a NaN variance becomes 0, an infinite one stays)
-    if (!(fabs(sum) < INFINITY) || !(var < INFINITY)) {  // ExactSum::add would throw (exact_sum.hpp:34)
-      atomicAdd(&overflow_s, 1u);
-      sum = var = 0.0;
+    if (scalars) {
+      if (!(fabs(sum) < INFINITY) || !(var < INFINITY)) {  // ExactSum::add would throw (exact_sum.hpp:34)
+        atomicAdd(&overflow_s, 1u);
+        sum = var = 0.0;
+      }
+      exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
     }
-    exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
 
     bool all_axes;
     active = cw.next(a, T, all_axes);
@@ -564,7 +585,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       peer_acc = cluster.map_shared_rank(acc, crank ^ 1u);
     }
     const std::uint32_t* peer_bins = peer_acc + kScalarAccs * kLaneCopies * kXWords;
-    const int ncells = static_cast<int>(a.bin_axes * nb);
+    const int ncells = static_cast<int>(a.bin_n * nb);
     const int nbw = ncells * kXWords;
     const int b0 = csize == 2 ? (crank ? nbw / 2 : 0) : 0, b1 = csize == 2 ? (crank ? nbw : nbw / 2) : nbw;
     for (int i = b0 + tid; i < b1; i += nt) {
@@ -573,11 +594,12 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
       if (!v) continue;
       const int c = i / kXWords, w = i - c * kXWords;
       const int ax = c / static_cast<int>(nb), cell = c - ax * static_cast<int>(nb);
-      const int slot = ax * static_cast<int>(a.nb_out) + min(cell, static_cast<int>(a.nb_out) - 1);
+      const int slot = (static_cast<int>(a.bin_lo) + ax) * static_cast<int>(a.nb_out) +
+                       min(cell, static_cast<int>(a.nb_out) - 1);
       add_word(static_cast<std::ptrdiff_t>(kScalarAccs + slot) * kXWords + w, v);
     }
     // est+/est-/var: the 32 lane copies (of both CTAs) folded into u64 word sums (< 2^38, exact)
-    const int nsw = kScalarAccs * kXWords;
+    const int nsw = scalars ? kScalarAccs * kXWords : 0;  // later passes deposit bins only
     const int s0 = csize == 2 ? (crank ? nsw / 2 : 0) : 0, s1 = csize == 2 ? (crank ? nsw : nsw / 2) : nsw;
     for (int i = s0 + tid; i < s1; i += nt) {
       const int kind = i / kXWords, w = i % kXWords;
@@ -599,7 +621,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     if (tid == 0 && cubes_s) add_word(-2, cubes_s * a.p - nonfinite_s);
     if (csize == 2) cluster.sync();  // the partner has finished reading this CTA's accumulators
   }
-  if (npeers) {
+  if (npeers && a.publish) {
     // Publish "this rank's words are in": every thread's reductions are
     // ordered before the block's arrival (fence.sc.sys + barrier); the last
     // block to arrive releases the iteration's flag into every rank's slot.

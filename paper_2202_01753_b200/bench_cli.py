@@ -12,8 +12,10 @@ sweep:     --runs seeded runs per tolerance level; tau starts at --tau-rel and i
            seed + level*runs + i (mcubes_bench.cpp:145-165)
 summarize: per-(integrand, dims, tau) run counts, convergence rate and R-7
            quartiles of rel_error over converged runs (mcubes_bench.cpp:192-244)
-scale:     (B200 addition, BASELINE config 5) one adjusting iteration per
-           (d, ncall) cell; evals/s device throughput and whole-run wall time.
+scale:     (B200 addition, BASELINE config 5) per (d, ncall) cell at the launch's
+           GPU count (torchrun for N > 1): one adjusting iteration's device
+           throughput, a whole-run wall time, and the reference CPU iteration
+           on the host cores beside it (gpus, cpu_* columns).
 Usage and I/O errors exit 1.
 """
 from __future__ import annotations
@@ -158,13 +160,61 @@ def cmd_summarize(path: str, out_path: Optional[str]) -> int:
     return 0
 
 
-def cmd_scale(o) -> int:
-    """BASELINE config 5: throughput over d x ncall (one adjusting iteration
-    per cell, device-timed through the stepped run; plus whole-run wall time
-    of an itmax=5/ita=3 integrate at the cell)."""
-    ctx = M.default_context()
-    out = _Out(o.out)
-    out.write("integrand,dims,maxcalls,g,m,p,evals_per_iteration,iteration_ms,evals_per_s,run5_wall_ms")
+def _scale_dist():
+    """(world, rank, dist module or None): torchrun sets WORLD_SIZE/RANK; one
+    process per GPU, NCCL (MCB_DIST_BACKEND=gloo lets ranks share a GPU)."""
+    import os
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1:
+        return 1, 0, None
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    if not dist.is_initialized():
+        backend = os.environ.get("MCB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            dist.init_process_group(backend)
+    return world, dist.get_rank(), dist
+
+
+def cmd_scale(o, cpu_timer=None) -> int:
+    """BASELINE config 5: throughput over d x ncall at the launch's GPU count.
+
+    Per cell: one adjusting iteration device-timed through the stepped run
+    (each rank samples its slice of the cube walk, the exact exchange is
+    all-reduced, max over ranks) and the wall time of a whole itmax=5/ita=3
+    integrate (dist.integrate when gpus > 1).  Launch with torchrun for
+    gpus > 1; rank 0 writes the CSV.  The cpu_* columns are filled when a
+    caller passes `cpu_timer(integrand, dims, maxcalls) -> (threads, ms)`
+    timing the reference CPU iteration on the host cores in the same run
+    (bench.py --scale does, with the compiled reference); the library itself
+    never runs a CPU path."""
+    import torch
+
+    world, rank, dist = _scale_dist()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)
+    ctx = M.Context(dev.index)
+    ctx.set_stream(stream.cuda_stream)
+    if rank != 0:
+        cpu_timer = None
+    out = _Out(o.out) if rank == 0 else None
+    if out:
+        out.write("integrand,dims,maxcalls,g,m,p,gpus,evals_per_iteration,iteration_ms,evals_per_s,run5_wall_ms,"
+                  "cpu_threads,cpu_iteration_ms,cpu_evals_per_s,speedup")
+
+    def max_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for d in [int(x) for x in o.dims.split(",")]:
         for nc in [int(float(x)) for x in o.ncalls.split(",")]:
             spec = M.make_integrand(o.integrand, d) if o.integrand not in ("fA", "fB") else M.make_integrand(
@@ -175,21 +225,55 @@ def cmd_scale(o) -> int:
             cfg = M.RunConfig(dims=d_eff, maxcalls=nc, itmax=3, ita=3, tau_rel=1e-15, lower=spec.lower,
                               upper=spec.upper, rng=o.rng)
             sp = M.setup(cfg)
-            run = M.Run(spec, cfg, ctx)
-            run.step(1)  # warm
-            ctx.synchronize()
-            t0 = time.perf_counter()
-            run.step(2)
-            ctx.synchronize()
-            it_ms = 1e3 * (time.perf_counter() - t0)
-            run.close()
+            with torch.cuda.stream(stream):
+                run = M.Run(spec, cfg, ctx)
+                m = run.work_items
+                n0, n1 = rank * m // world, (rank + 1) * m // world
+                x = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
+                run.set_exchange(x.data_ptr())
+
+                def step(it):
+                    run.sample(it, n0, n1)
+                    run.reduce(it)
+                    if dist is not None:
+                        dist.all_reduce(x[:run.exchange_words(it)])
+                    run.finish(it)
+
+                step(1)  # warm
+                torch.cuda.synchronize()
+                if dist is not None:
+                    dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step(2)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                it_ms = max_ranks(e0.elapsed_time(e1))
+                run.close()
             cfg5 = M.RunConfig(dims=d_eff, maxcalls=nc, itmax=5, ita=3, tau_rel=1e-15, lower=spec.lower,
                                upper=spec.upper, rng=o.rng)
-            _, run_ms = _timed(spec, cfg5, ctx)
+            with torch.cuda.stream(stream):
+                if dist is None:
+                    _, run_ms = _timed(spec, cfg5, ctx)
+                else:
+                    from . import dist as mdist
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    t0 = time.perf_counter()
+                    mdist.integrate(spec, cfg5, ctx=ctx)
+                    run_ms = max_ranks(1e3 * (time.perf_counter() - t0))
             ev = sp.m * sp.p
-            out.write(",".join(str(x) for x in [spec.name, d_eff, nc, sp.g, sp.m, sp.p, ev, fmt17(it_ms),
-                                                fmt17(ev / (it_ms * 1e-3)), fmt17(run_ms)]))
-    out.close()
+            cpu_cols = ["", "", "", ""]
+            if cpu_timer is not None and ev <= o.cpu_max_evals:
+                timed = cpu_timer(o.integrand, d_eff, nc)
+                if timed:
+                    threads, cms = timed
+                    cpu_cols = [str(threads), fmt17(cms), fmt17(ev / (cms * 1e-3)), fmt17(cms / it_ms)]
+            if out:
+                out.write(",".join(str(v) for v in [spec.name, d_eff, nc, sp.g, sp.m, sp.p, world, ev, fmt17(it_ms),
+                                                    fmt17(ev / (it_ms * 1e-3)), fmt17(run_ms)] + cpu_cols))
+    if out:
+        out.close()
     return 0
 
 
@@ -225,6 +309,9 @@ def main(argv=None) -> int:
     scale.add_argument("--dims", default="2,4,6,8,10")
     scale.add_argument("--ncalls", default="1e6,1e8,1e10")
     scale.add_argument("--rng", choices=["compat", "philox"], default="compat")
+    scale.add_argument("--cpu-max-evals", type=float, default=1e9,
+                       help="with a CPU timer (bench.py --scale): time the reference CPU iteration for cells "
+                            "with m*p up to this")
     scale.add_argument("--out", default=None)
     try:
         o = ap.parse_args(argv)

@@ -130,10 +130,44 @@ def test_sweep_schedule(tmp_path):
 
 @pytest.mark.gpu
 def test_scale_subcommand(tmp_path):
+    """bench.py --scale: the CLI's scale sweep with the reference CPU column
+    filled in the same run (the library never runs a CPU path itself)."""
     out = tmp_path / "scale.csv"
-    r = run(["scale", "--integrand", "f4", "--dims", "3,8", "--ncalls", "1e6,1e8", "--out", str(out)])
+    r = subprocess.run([sys.executable, "bench.py", "--scale", str(out), "--scale-dims", "3,8",
+                        "--scale-ncalls", "1e6,1e8"], capture_output=True, text=True, cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stderr
     lines = out.read_text().splitlines()
+    head = lines[0].split(",")
     assert len(lines) == 5 and lines[0].startswith("integrand,dims,maxcalls")
+    col = {k: i for i, k in enumerate(head)}
     for ln in lines[1:]:
-        assert float(ln.split(",")[8]) > 1e8  # evals/s
+        f = ln.split(",")
+        assert int(f[col["gpus"]]) == 1
+        assert float(f[col["evals_per_s"]]) > 1e8
+        # the reference CPU iteration on the host cores, in the same run
+        assert int(f[col["cpu_threads"]]) >= 1 and float(f[col["cpu_evals_per_s"]]) > 0
+        assert float(f[col["speedup"]]) > 1
+
+
+@pytest.mark.gpu
+def test_scale_subcommand_multi_rank(tmp_path):
+    """The scale sweep under torchrun (world 2 sharing cuda:0 over gloo):
+    the gpus column and the same cells."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "scale2.csv"
+    env = dict(os.environ, MCB_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "-m",
+                        "paper_2202_01753_b200.bench_cli", "scale", "--integrand", "f4", "--dims", "4",
+                        "--ncalls", "1e7", "--out", str(out)],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = out.read_text().splitlines()
+    assert len(lines) == 2
+    f = dict(zip(lines[0].split(","), lines[1].split(",")))
+    assert f["gpus"] == "2" and float(f["evals_per_s"]) > 1e8

@@ -48,13 +48,15 @@ def _ref_grid(fam, d, its=3):
 
 
 def _gpu(ctx, fam, d, edges, sp, seed, it, mode="all", rng="compat"):
+    """rng: compat | philox (24-bit bin addends) | philox_exact (exact bins)."""
     f = M.make_suite_integrand(fam, d)
     g = M.Grid.from_edges(d, 50, [0.0] * d, [1.0] * d, edges)
+    stream, bins = ("philox", "exact") if rng == "philox_exact" else (rng, "")
     if mode == "frozen":
-        r = M.v_sample_no_adjust(f, g, sp.m, 1, sp.p, seed, it, rng=rng, ctx=ctx)
+        r = M.v_sample_no_adjust(f, g, sp.m, 1, sp.p, seed, it, rng=stream, ctx=ctx)
         return r.raw_estimate, r.raw_variance, None, None
     bu = M.BinUpdate.axis0_only if mode == "axis0" else M.BinUpdate.all_axes
-    r = M.v_sample(f, g, sp.m, 1, sp.p, seed, it, bu, rng=rng, ctx=ctx)
+    r = M.v_sample(f, g, sp.m, 1, sp.p, seed, it, bu, rng=stream, bins=bins, ctx=ctx)
     return r.raw_estimate, r.raw_variance, r.contributions.values, r.contributions.writes()
 
 
@@ -100,14 +102,16 @@ def test_row_mode_compat_modes_bitwise_vs_reference(ctx, d, maxcalls, mode):
     _check(got, want, d, sp, mode)
 
 
+@pytest.mark.parametrize("rng", ["philox", "philox_exact"])
 @pytest.mark.parametrize("d,maxcalls", [(8, 10 ** 8), (5, 8 * 10 ** 7), (4, 3 * 10 ** 8), (6, 2 * 10 ** 8)])
-def test_row_mode_philox_bitwise_vs_c_twin(ctx, d, maxcalls):
-    """The north-star Philox path in row mode against its threaded C twin."""
+def test_row_mode_philox_bitwise_vs_c_twin(ctx, d, maxcalls, rng):
+    """The north-star Philox path in row mode against its threaded C twin,
+    with 24-bit and with exact bin addends."""
     sp = _shape(d, maxcalls)
     edges = _ref_grid(2, d)
-    got = _gpu(ctx, 2, d, edges, sp, 9, 3, rng="philox")
+    got = _gpu(ctx, 2, d, edges, sp, 9, 3, rng=rng)
     want = O.v_sample("orc", 2, None, d, 50, [0.0] * d, [1.0] * d, edges, sp.m, sp.s, sp.p, 9, 3, "all", THREADS,
-                      rng="philox")
+                      rng=rng)
     _check(got, want, d, sp)
 
 
