@@ -306,12 +306,13 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- the headline: device-timed steps with inputs resident in HBM
     clocks = ClockSampler(gpu) if rank == 0 else None
-    head = measure(args.maxcalls, args.rng, args.bins, args.steps, args.warmup, clocks=clocks)
+    bins = args.bins if args.rng == "philox" else ""  # compat always sums exact bins
+    head = measure(args.maxcalls, args.rng, bins, args.steps, args.warmup, clocks=clocks)
     m, p = head["m"], head["p"]
     res = head["result"]
 
     # ---- end to end through the C ABI with host buffers (H2D grid in, D2H adapted grid out)
-    run2, xbuf2, _, n0, n1 = make_run(args.maxcalls, args.rng, args.bins, args.warmup + args.steps, 1)
+    run2, xbuf2, _, n0, n1 = make_run(args.maxcalls, args.rng, bins, args.warmup + args.steps, 1)
     host_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
     host_edges[:] = np.asarray(M.Grid(DIMS, N_BINS, [0.0] * DIMS, [1.0] * DIMS).raw_edges)
     out_edges = torch.empty(DIMS * N_BINS, dtype=torch.float64).pin_memory().numpy()
@@ -408,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
             line["compat"] = secondary(args.maxcalls, "compat", "", args.steps,
                                        "the same steps on the reference's own stream and arithmetic order "
                                        "(bitwise the reference)")
-        line["maxcalls_1e10"] = secondary(MAXCALLS_LARGE, args.rng, args.bins, min(args.steps, 5),
+        line["maxcalls_1e10"] = secondary(MAXCALLS_LARGE, args.rng, bins, min(args.steps, 5),
                                           "GPU-only: 8D f4 at maxcalls 1e10 (m = 16^8 = 2^32 sub-cubes)")
 
     if rank == 0 and world == 1 and not args.no_cpu:

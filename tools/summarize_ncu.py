@@ -98,7 +98,7 @@ def main():
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get("dram__bytes_read.sum", "byte"), 1)
     with open(os.path.join(ROOT, "profiles", f"ncu_k1_{tag}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    # per-stream entry (vsample_kernel<F, D, Rng, NB>: Rng 1 = philox, 0 = compat), read by bench.py
+    # per-stream entry (vsample_kernel<F, D, Rng, NB>), read by bench.py
     tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
     try:
         table = json.load(open(tf))
@@ -107,7 +107,9 @@ def main():
     except (OSError, ValueError):
         table = {}
     targs = [a.strip() for a in name.split("<", 1)[1].split(">", 1)[0].split(",")] if "<" in name else []
-    rng = "philox" if len(targs) > 2 and targs[2] == "1" else "compat"
+    kind = targs[2] if len(targs) > 2 else "0"  # RngKind: 0 compat, 1 philox (r24 bins), 2 philox_exact
+    kind = kind.replace("(mcubes::gpu::RngKind)", "")
+    rng = {"1": "philox_r24", "2": "philox_exact"}.get(kind, "compat")
     winst = float(m.get("smsp__inst_executed.sum", 0) or 0)
     table[rng] = {"bytes_per_launch": dram * scale, "source": f"profiles/ncu_k1_{tag}.md", "kernel": name,
                   "warp_instr_per_eval": (winst / evals) if (evals and winst) else None}
