@@ -353,6 +353,8 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
                                   std::to_string(ctx.max_smem()) + " B)");
     passes = (bin_axes + most - 1) / most;
     per_pass = (bin_axes + passes - 1) / passes;  // balanced
+    if constexpr (NB != 0)  // the compile-time-n_bins kernels run one pass (see vsample_kernel)
+      return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);
   }
   L.passes = passes;
   L.smem = sample_smem_bytes(D, L.pnb, per_pass);

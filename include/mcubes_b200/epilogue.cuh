@@ -6,7 +6,7 @@
 // exchange buffer (unnormalised u64 digit sums: integer, so exact and
 // order-free; under multi-GPU this buffer is what NCCL all-reduces) -- it makes
 // one m-Cubes iteration with no host round trip.  The finish kernel rounds each accumulator to
-// the nearest double exactly like ExactSum::value() (exact_sum.hpp:137-179),
+// the nearest double exactly like ExactSum::value() (exact_sum.hpp:65-109),
 // producing v_sample's outputs (sampler.hpp:322-332), then replaces
 // Grid::adjusted / adjusted_symmetric (grid.hpp:104-146, 232-297),
 // weighted_estimate and check_convergence (driver.hpp:146-178) and the loop
@@ -117,7 +117,7 @@ __device__ inline void adjust_axis_warp(double* edges_g, const double* edges_in,
   __syncwarp();
   MCB_ADJ_STAMP(2);
   if (lane == 0) {  // the reference's sequential accumulations, in its order
-    // rtot (grid.hpp:603-613) and the walk's cum (grid.hpp:623-626) add the
+    // rtot (grid.hpp:252-264) and the walk's cum (grid.hpp:268-278) add the
     // same imp[] in the same order, so one pass yields both: P[n] == rtot.
     // (imp is loaded eight at a time ahead of the stores into P: the compiler
     // cannot move a load above a possibly aliasing shared store, which would

@@ -32,6 +32,7 @@ namespace mcubes::gpu::exact {
 /// Digits of |v| * 2^1074: word index and the three radix-2^32 digits.
 struct Digits {
   std::uint32_t w, d0, d1, d2;
+  std::uint32_t be;  ///< biased exponent field (0x7ff: the addend was +-inf -- ExactSum::add throws)
 };
 
 MCB_HD bool split(double v, Digits& out) {
@@ -42,6 +43,7 @@ MCB_HD bool split(double v, Digits& out) {
   std::memcpy(&bits, &v, 8);
 #endif
   bits &= 0x7fffffffffffffffull;
+  out.be = static_cast<std::uint32_t>(bits >> 52);
   if (!bits) return false;
   const std::uint32_t hi = static_cast<std::uint32_t>(bits >> 32);
   const std::uint32_t lo = static_cast<std::uint32_t>(bits);
@@ -134,11 +136,10 @@ __device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::u
 /// Two digits of RN24(|v|) * 2^1074 (round-half-up on the 53-bit significand).
 struct Digits2 {
   std::uint32_t w, d0, d1;
+  std::uint32_t be;  ///< biased exponent after rounding (0x7ff: +-inf, or rounded up to 2^1024)
 };
 
 inline constexpr int kBinDrop = 29;  ///< significand bits dropped: 53 - 24
-/// Smallest double that RN24 (round_bin_bits) rounds up to 2^1024.
-inline constexpr double kR24Max = 0x1.ffffffp+1023;
 
 MCB_HD std::uint64_t round_bin_bits(std::uint64_t bits) {
   return (bits + (1ull << (kBinDrop - 1))) & ~((1ull << kBinDrop) - 1);  // carries into the exponent
@@ -152,10 +153,12 @@ MCB_HD bool split_r24(double v, Digits2& out) {
   std::memcpy(&bits, &v, 8);
 #endif
   bits &= 0x7fffffffffffffffull;
+  out.be = 0;
   if (!bits) return false;
   bits = round_bin_bits(bits);
   const std::uint32_t hi = static_cast<std::uint32_t>(bits >> 32);
   const std::uint32_t be = hi >> 20;
+  out.be = be;
   // 24-bit significand m = (implicit:hi[19:0]:lo[31:29]), its LSB at bit pos + 29
   const std::uint32_t m = (((hi & 0x000FFFFFu) | (be ? 0x00100000u : 0u)) << 3) |
                           (static_cast<std::uint32_t>(bits) >> kBinDrop);
@@ -320,7 +323,7 @@ __device__ __forceinline__ void add_shared2_s(std::uint32_t a_s, double a, std::
 #endif
 
 /// Round the exact integer (pos - neg) * 2^-1074 to the nearest double, ties
-/// to even -- ExactSum::value() (exact_sum.hpp:137-179).  Inputs are
+/// to even -- ExactSum::value() (exact_sum.hpp:65-109).  Inputs are
 /// unnormalised u64 digit sums (the exchange format); neg may be null.
 MCB_HD double round_words(const unsigned long long* pos, const unsigned long long* neg) {
   std::uint32_t a[kXWords], b[kXWords];
@@ -360,7 +363,7 @@ MCB_HD double round_words(const unsigned long long* pos, const unsigned long lon
     const std::uint64_t v = static_cast<std::uint64_t>(big[0]) | (static_cast<std::uint64_t>(big[1]) << 32);
     r = std::ldexp(static_cast<double>(v), -1074);  // exact (sub)normal
   } else {
-    // 53-bit window [top-52, top], guard bit, sticky (exact_sum.hpp:160-176)
+    // 53-bit window [top-52, top], guard bit, sticky (exact_sum.hpp:91-104)
     const int lo = top - 52;
     const int wi = lo >> 5, sh = lo & 31;
     std::uint64_t mant = static_cast<std::uint64_t>(big[wi]) >> sh;
@@ -465,7 +468,7 @@ __device__ __forceinline__ unsigned long long digit(const unsigned long long (&v
 }  // namespace warpx
 
 /// Warp-cooperative form of round_words: RN-even of (pos - neg) * 2^-1074
-/// (ExactSum::value(), exact_sum.hpp:137-179).  All 32 lanes call it; every
+/// (ExactSum::value(), exact_sum.hpp:65-109).  All 32 lanes call it; every
 /// lane returns the result.
 __device__ __forceinline__ double warp_round_words(const unsigned long long* pos, const unsigned long long* neg) {
   const int lane = threadIdx.x & 31;

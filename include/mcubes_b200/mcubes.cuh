@@ -214,7 +214,7 @@ class Grid {
     }
   }
 
-  /// From raw edges (validated like Grid::read, grid.hpp:530-548).
+  /// From raw edges (validated like Grid::read, grid.hpp:161-175).
   static Grid from_edges(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> lower,
                          std::vector<double> upper, std::vector<double> edges) {
     if (dims == 0 || n_bins < 2) throw std::invalid_argument("Grid::read: malformed header");

@@ -399,8 +399,17 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   const std::uint32_t var_s = acc_s + (2 * kLaneCopies + lane) * kAccBytes;
   const std::uint32_t bins_s = acc_s + kScalarAccs * kLaneCopies * kAccBytes;
   const std::uint32_t end_s = acc_s + static_cast<std::uint32_t>(nacc) * kAccBytes;
-  const std::uint32_t bin_n = a.bin_n, bin_lo = a.bin_lo;
-  const bool scalars = a.scalars != 0;
+  // The compile-time-n_bins kernels (NB != 0) run every shape in one pass
+  // (launch_k1 sends multi-pass shapes to NB = 0), so their pass logic folds away.
+  constexpr bool kOnePass = NB != 0;
+  const std::uint32_t bin_n = kOnePass ? a.bin_axes : a.bin_n, bin_lo = kOnePass ? 0u : a.bin_lo;
+  const bool scalars = kOnePass || a.scalars != 0;
+  // An exact addend that overflowed to +-inf ((f J)^2, a cube's sum or
+  // variance): the reference's ExactSum::add throws (exact_sum.hpp:34).  Its
+  // digits are deposited like any other (they stay inside the accumulator);
+  // the flag is counted once per thread at the end and the finish kernel
+  // stops the run with that error.
+  bool ovf = false;
   constexpr std::uint32_t kCell = 4u * kXWords;  // bytes per accumulator
 
   // sampler.hpp:173-176: the same (f J)^2 on every axis -- split it once,
@@ -413,15 +422,11 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     Dg dgt;
     bool nz;
     const double sq = __dmul_rn(fj, fj);
-    // (f J)^2 overflowed (|f J| > ~1.3e154; with 24-bit addends also a value
-    // that RN24 rounds up to 2^1024): the reference's ExactSum::add throws
-    // (exact_sum.hpp:34) -- count it, the finish kernel stops the run
-    if (!(sq < (kR24 ? exact::kR24Max : INFINITY))) {
-      atomicAdd(&overflow_s, 1u);
-      return;
-    }
     if constexpr (kR24) nz = exact::split_r24(sq, dgt);
     else nz = exact::split(sq, dgt);
+    // (f J)^2 overflowed (|f J| > ~1.3e154; with 24-bit addends also a value
+    // that RN24 rounds up to 2^1024)
+    ovf |= dgt.be == 0x7ffu;
     if (nz) {
       const std::uint32_t wb = bins_s + 4u * dgt.w;
       if (bin_n == static_cast<std::uint32_t>(D)) {  // every axis in one pass (the common case)
@@ -438,7 +443,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
           if constexpr (kR24) exact::add_digits2_s<D>(ad, end_s, dgt);
           else exact::add_digits_s<D>(ad, end_s, dgt);
         }
-      } else if (bin_n == 1 && bin_lo == 0) {  // BinUpdate::axis0_only
+      } else if (kOnePass || (bin_n == 1 && bin_lo == 0)) {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
         if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
         else exact::add_digits_s<1>(ad, end_s, dgt);
@@ -527,10 +532,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     }
     if (!(var > 0.0)) var = 0.0;  // sampler.hpp:179 (a NaN variance becomes 0, an infinite one stays)
     if (scalars) {
-      if (!(fabs(sum) < INFINITY) || !(var < INFINITY)) {  // ExactSum::add would throw (exact_sum.hpp:34)
-        atomicAdd(&overflow_s, 1u);
-        sum = var = 0.0;
-      }
+      ovf |= !(fabs(sum) < INFINITY) || !(var < INFINITY);  // ExactSum::add would throw (exact_sum.hpp:34)
       exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
     }
 
@@ -544,6 +546,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     }
   }
   MCB_K1_STAMP(3, atomicMin)
+  if (ovf) atomicAdd(&overflow_s, 1u);
   {  // the block's visited-cube count (warp sums in u64: a thread's count fits u32, a block's may not)
     unsigned long long c = ncubes;
 #pragma unroll

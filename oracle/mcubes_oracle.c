@@ -231,7 +231,7 @@ static int make_fn(orc_fn* f, int id, const double* params, uint32_t nparams, ui
   f->d = d;
   f->params = params;
   f->nparams = nparams;
-  f->fb_norm = pow(2.0 * 3.141592653589793 * 0.01, -4.5); /* integrands.hpp:467 */
+  f->fb_norm = pow(2.0 * 3.141592653589793 * 0.01, -4.5); /* integrands.hpp:207 */
   if ((id >= 1 && id <= 9) || (id >= 32 && id <= 37)) {
     if (id == 9) {
       if (nparams < 1) return fail(-1, "table integrand needs params");

@@ -34,7 +34,7 @@ IntegrandOps ops_F6(int, RngKind r, const BuiltinArgs&) { return both(r, fn::F6{
 IntegrandOps ops_FA(int, RngKind r, const BuiltinArgs&) { return both(r, fn::FA{}); }
 #elif MCB_INST == 8
 IntegrandOps ops_FB(int, RngKind r, const BuiltinArgs&) {
-  // integrands.hpp:466-467, evaluated on the host exactly as the reference does
+  // integrands.hpp:206-207, evaluated on the host exactly as the reference does
   const double sigma2 = 0.01;
   return both(r, fn::FB{std::pow(2.0 * 3.141592653589793 * sigma2, -4.5)});
 }

@@ -33,6 +33,13 @@ D, MAXCALLS, SEEDS = 8, 10 ** 9, range(100, 116)
 STREAMS = {"compat": ("compat", ""), "philox_r24": ("philox", "r24"), "philox_exact": ("philox", "exact")}
 
 
+def _chi2_dof(history):
+    """chi^2/dof of a run of iterations about their weighted mean (driver.hpp:146-169)."""
+    w = [1.0 / h.variance for h in history]
+    mean = sum(wi * h.estimate for wi, h in zip(w, history)) / sum(w)
+    return sum((h.estimate - mean) ** 2 / h.variance for h in history) / max(1, len(history) - 1)
+
+
 def _runs(ctx, fam, itmax, ita, tau):
     f = M.make_suite_integrand(fam, D)
     out = {}
@@ -49,14 +56,17 @@ def test_pulls_and_combined_estimates_match_reference_stream(ctx, fam):
     truth = f.reference
     stats = {}
     for name, rr in runs.items():
+        # iterations 2..6: iteration 1 samples the uniform grid, where a peaked
+        # integrand's variance estimate is unreliable on every stream
         pulls = [(h.estimate - truth) / math.sqrt(h.variance) for r in rr for h in r.history[1:]]
         stats[name] = (statistics.fmean(pulls), statistics.pstdev(pulls),
-                       statistics.fmean(r.chi2_dof for r in rr))
-        mean, sd, chi2 = stats[name]
+                       statistics.fmean(_chi2_dof(r.history[1:]) for r in rr))
         assert len(pulls) == 5 * len(SEEDS)
-        assert abs(mean) < 0.45, (name, stats[name])  # 80 pulls: standard error 0.11
-        assert 0.7 < sd < 1.35, (name, stats[name])
-        assert 0.4 < chi2 < 1.8, (name, stats[name])
+    for name, (mean, sd, chi2) in stats.items():
+        assert abs(mean) < 0.45, stats  # 80 pulls: standard error 0.11
+        assert 0.7 < sd < 1.35, stats
+        assert 0.5 < chi2 < 1.6, stats  # 16 seeds x 4 dof: standard error of the mean 0.18
+    for name, rr in runs.items():
         # the combined estimate against the analytic value
         assert sum(abs(r.estimate - truth) <= 3 * r.sigma for r in rr) >= 15, name
         # device-counted samples: every iteration sampled every cube p times

@@ -77,13 +77,13 @@ def main():
     agg = defaultdict(float)
     cur, ie = None, None
     for r in src:
-        if len(r) >= 2 and r[0] == "File Path":
+        if len(r) == 2 and r[0] == "File Path":
             cur = r[1].split("/")[-1]
             continue
-        if len(r) > 2 and r[0] == "Line No":
+        if r and r[0] == "Line No":
             ie = r.index("Instructions Executed")
             continue
-        if ie is not None and len(r) > ie and r[0].isdigit():
+        if ie is not None and len(r) > ie and r[0].isdigit():  # cuda rows carry their line's total
             try:
                 agg[cur] += float(r[ie])
             except ValueError:
