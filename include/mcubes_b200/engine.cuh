@@ -299,6 +299,7 @@ struct Launch {
   std::size_t smem = 0;
   std::uint32_t pnb = 0;  ///< histogram cells per axis (n_bins, +1 padding cell on the Philox path)
   std::uint32_t passes = 1;  ///< bin passes (> 1 when the histograms exceed one CTA's shared memory)
+  std::uint32_t copies = 1;  ///< grid-table copies in shared memory (stage_grid)
 };
 
 /// Cells per axis in K1's shared histogram for a stream kind.
@@ -340,9 +341,8 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   // CTA's shared memory, the axes are split over passes that re-sample the
   // same keyed points (SampleArgs::bin_lo/bin_n); results are bitwise those of
   // one pass.
-  const auto fits = [&](std::uint32_t na) {
-    return sample_smem_bytes(D, L.pnb, na) <= static_cast<std::size_t>(ctx.max_smem());
-  };
+  const std::size_t budget = std::min<std::size_t>(kK1SmemBudget, static_cast<std::size_t>(ctx.max_smem()));
+  const auto fits = [&](std::uint32_t na) { return sample_smem_bytes(D, L.pnb, na) <= budget; };
   std::uint32_t passes = 1, per_pass = bin_axes;
   if (!fits(bin_axes)) {
     std::uint32_t most = bin_axes;
@@ -357,7 +357,17 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
       return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);
   }
   L.passes = passes;
-  L.smem = sample_smem_bytes(D, L.pnb, per_pass);
+  // grid-table copies: fixed per instantiation for the compile-time-n_bins
+  // kernels (they fit by construction), else the most that fit this pass
+  if constexpr (NB != 0) {
+    L.copies = fixed_tab_copies(D, L.pnb);
+    if (sample_smem_bytes(D, L.pnb, per_pass, L.copies) > budget)
+      return launch_k1<F, D, R, 0>(ctx, f, sh, bin_axes, iter_root, n0, n1, stop, err_key, words);
+  } else {
+    L.copies = MCB_K1_TAB_COPIES_MAX;
+    while (L.copies > 1 && sample_smem_bytes(D, L.pnb, per_pass, L.copies) > budget) L.copies >>= 1;
+  }
+  L.smem = sample_smem_bytes(D, L.pnb, per_pass, L.copies);
   // attribute + occupancy queries are cached per instantiation (host latency
   // matters for small-ncall iterations)
   thread_local std::size_t cached_smem = 0;
@@ -442,6 +452,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   if (!words) throw std::invalid_argument("K1: the exchange buffer must be provided");
   a.words = words;
   a.nb_out = sh.nb;
+  a.tab_copies = L.copies;
   a.err_key = err_key;
   a.stop = stop;
   a.peer = ctx.peer;
@@ -455,7 +466,7 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
     a.bin_n = std::min(per_pass, bin_axes - a.bin_lo);
     a.scalars = q == 0 ? 1u : 0u;
     a.publish = q + 1 == passes ? 1u : 0u;
-    const std::size_t smem = sample_smem_bytes(D, L.pnb, a.bin_n);
+    const std::size_t smem = sample_smem_bytes(D, L.pnb, a.bin_n, L.copies);
     launch_pdl_cluster(kern, L.blocks, threads, smem, ctx.stream(), cluster, a, f);
     ++ctx.launches;
   }

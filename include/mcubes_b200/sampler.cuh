@@ -83,23 +83,32 @@ struct SampleArgs {
   unsigned long long* words;  ///< exchange accumulators (zeroed): every block adds its nonzero words here;
                               ///< words[-3..-1]: overflowed addends, finite and non-finite samples (kXHeader)
   std::uint32_t nb_out;       ///< n_bins of the exchange layout (the padding cell folds into bin nb_out-1)
+  std::uint32_t tab_copies;   ///< copies of the grid table in shared memory (runtime-n_bins kernels; 0 = 1)
   unsigned long long* err_key;  ///< min over non-finite samples of t*p + k (init all-ones)
   const int* stop;              ///< nullable; nonzero = run finished, skip
   PeerArgs peer;                ///< multi-GPU exchange over peer memory (peer.npeers == 0: local words)
 };
 
 /// Accumulator slots in one block's partial.
-MCB_HD int block_accs(std::uint32_t bin_axes, std::uint32_t nb) {
+MCB_HD constexpr int block_accs(std::uint32_t bin_axes, std::uint32_t nb) {
   return kScalarAccs * kLaneCopies + static_cast<int>(bin_axes * nb);
 }
 
-/// Dynamic shared memory of K1 for a given shape.
-MCB_HD std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes) {
-  const std::size_t grid = 2 * sizeof(double) * static_cast<std::size_t>(D) * nb;  // {left, width}
+/// Dynamic shared memory of K1 for a given shape, with `copies` interleaved
+/// copies of the grid table (see stage_grid).
+MCB_HD constexpr std::size_t sample_smem_bytes(int D, std::uint32_t nb, std::uint32_t bin_axes, std::uint32_t copies = 1) {
+  const std::size_t grid = 2 * sizeof(double) * static_cast<std::size_t>(D) * nb * copies;  // {left, width}
   const std::size_t rcp = sizeof(double) * kRcpSmem;
   std::size_t acc = sizeof(std::uint32_t) * static_cast<std::size_t>(block_accs(bin_axes, nb)) * kXWords;
   acc = (acc + 15) & ~std::size_t{15};
   return grid + rcp + acc;
+}
+
+/// 128-bit shared load at a 32-bit shared-window byte address.
+__device__ __forceinline__ double2 lds_d2(std::uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
 }
 
 /// Correctly rounded a / b given y = RN(1/b) (Markstein).
@@ -109,19 +118,43 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
   return __fma_rn(r, y, q0);
 }
 
+/// Dynamic shared memory K1 may use (the opt-in maximum less a margin for
+/// its few static shared variables).
+inline constexpr std::size_t kK1SmemBudget = 227 * 1024 - 1024;
+
+/// Grid-table copies of the compile-time-n_bins kernels: the most (8, 4, 2)
+/// that fit next to every axis' histograms, else 1.
+#ifndef MCB_K1_TAB_COPIES_MAX
+#define MCB_K1_TAB_COPIES_MAX 8
+#endif
+constexpr std::uint32_t fixed_tab_copies(int D, std::uint32_t pnb) {
+  for (std::uint32_t c = MCB_K1_TAB_COPIES_MAX; c > 1; c >>= 1)
+    if (sample_smem_bytes(D, pnb, static_cast<std::uint32_t>(D), c) <= kK1SmemBudget) return c;
+  return 1;
+}
+
 template <int D>
 using DigitT = std::conditional_t<(D <= 2), std::uint64_t, std::uint32_t>;
 
 /// Stage the grid as per-bin {left edge, width} pairs (one 128-bit LDS per
 /// axis per sample).  width = right - left exactly as grid.hpp:218-219.
+///
+/// The table is stored C times, interleaved: entry e's copies fill C
+/// consecutive 16-byte slots, and lane l reads copy l mod C.  A 128-bit
+/// shared load is served a quarter-warp (8 lanes, 128 B) per wavefront; the
+/// 8 lanes of a quarter then always sit in 8 distinct bank groups whatever
+/// bins they hit, so a table lookup costs the minimum 4 wavefronts instead of
+/// ~9 for random bins in one copy (ncu: the table lookups were 54 % of a
+/// saturated shared-memory pipe).
 template <int D>
-__device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
+__device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a, std::uint32_t C) {
   const std::uint32_t nb = a.nb;
   for (std::uint32_t idx = threadIdx.x; idx < D * nb; idx += blockDim.x) {
     const std::uint32_t j = idx / nb, i = idx % nb;
     const double* row = a.edges + static_cast<std::size_t>(j) * nb;
     const double left = i == 0 ? a.lower[j] : row[i - 1];
-    LW[idx] = make_double2(left, __dsub_rn(row[i], left));
+    const double2 v = make_double2(left, __dsub_rn(row[i], left));
+    for (std::uint32_t c = 0; c < C; ++c) LW[idx * C + c] = v;
   }
 }
 
@@ -133,14 +166,15 @@ __device__ __forceinline__ void stage_grid(double2* LW, const SampleArgs& a) {
 /// needs no clamp -- its deposit lands in a padding cell that K1's flush folds into
 /// bin nb-1 (philox_pnb).
 template <int D>
-__device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a) {
+__device__ __forceinline__ void stage_grid_fast(double2* LW, const SampleArgs& a, std::uint32_t C) {
   const std::uint32_t nb = a.nb, pnb = nb + 1;
   for (std::uint32_t idx = threadIdx.x; idx < D * pnb; idx += blockDim.x) {
     const std::uint32_t j = idx / pnb, i0 = idx % pnb, i = i0 < nb ? i0 : nb - 1;
     const double* row = a.edges + static_cast<std::size_t>(j) * nb;
     const double left = i == 0 ? a.lower[j] : row[i - 1];
     const double w = __dsub_rn(row[i], left);
-    LW[idx] = make_double2(__fma_rn(-static_cast<double>(i), w, left), w);
+    const double2 v = make_double2(__fma_rn(-static_cast<double>(i), w, left), w);
+    for (std::uint32_t c = 0; c < C; ++c) LW[idx * C + c] = v;
   }
 }
 
@@ -162,9 +196,10 @@ __device__ __forceinline__ rng::U4 philox_rk(rng::U4 c, const std::uint32_t (&rk
 /// z = (digit + u) * nb / g as one FMA from the per-cube base; point and
 /// jacobian from the {A, width} table.  Returns f*J.
 template <class F, int D, int NB, class Dig>
-__device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, const double2* LW,
-                                                    const Dig (&dig)[D], std::uint64_t t, std::uint32_t k,
-                                                    double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
+__device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F& f, std::uint32_t lw_s,
+                                                    std::uint32_t C, const Dig (&dig)[D], std::uint64_t t,
+                                                    std::uint32_t k, double (&x)[D], std::uint32_t (&bin)[D],
+                                                    double& fx) {
   const std::uint32_t pnb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + 1;  // padded table (stage_grid_fast)
   std::uint32_t r[(D + 3) & ~3];
 #pragma unroll
@@ -185,12 +220,25 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
     // (digit < 2^21), so z is one I2F.U64 and one DMUL: z = RN((digit 2^32 + r) cs).
     double z;
     if constexpr (sizeof(Dig) == 4) {
+#if MCB_K1_ZASM
+      // the same bits without the I2F: 2^52 + digit:r is the double with words
+      // {0x43300000 | digit, r} (digit < 2^20); subtracting 2^52 is exact
+      z = __dmul_rn(__dadd_rn(__hiloint2double(static_cast<int>(0x43300000u | dig[j]), static_cast<int>(r[j])),
+                              -0x1p52),
+                    a.cs);
+#else
       z = __dmul_rn(__ull2double_rn((static_cast<std::uint64_t>(dig[j]) << 32) | r[j]), a.cs);
+#endif
     } else {
       z = __fma_rn(__uint2double_rn(r[j]), a.cs, __dmul_rn(__ull2double_rn(dig[j]), a.nbg));
     }
+#if MCB_K1_FLOOR
+    // floor(z) on the FP64 pipe: 2^52 + z rounded down has ulp 1, its low word is floor(z)
+    const std::uint32_t i = static_cast<std::uint32_t>(__double2loint(__dadd_rd(z, 0x1p52)));
+#else
     const std::uint32_t i = __double2uint_rz(z);  // 0 <= z <= nb: no clamp (padded table)
-    const double2 lw = LW[j * pnb + i];
+#endif
+    const double2 lw = lds_d2(lw_s + (static_cast<std::uint32_t>(j) * pnb + i) * C * 16u);  // lane's copy
     x[j] = __fma_rn(z, lw.y, lw.x);
     jw = j == 0 ? lw.y : __dmul_rn(jw, lw.y);
     bin[j] = i;
@@ -202,7 +250,7 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
 /// One sample: point, jacobian, bins and f*J of sample k of a cube
 /// (sampler.hpp:163-170 with transform_impl, grid.hpp:204-224).
 template <class F, int D, int NB>
-__device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, const double2* LW,
+__device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, std::uint32_t lw_s, std::uint32_t C,
                                                const double (&dg)[D], std::uint64_t croot, std::uint32_t k,
                                                double (&x)[D], std::uint32_t (&bin)[D], double& fx) {
   const std::uint32_t nb = NB ? static_cast<std::uint32_t>(NB) : a.nb, nbm1 = nb - 1;
@@ -219,7 +267,7 @@ __device__ __forceinline__ double sample_point(const SampleArgs& a, const F& f, 
     const double z = __dmul_rn(u, a.nbd);
     std::uint32_t i = __double2uint_rz(z);
     i = i < nbm1 ? i : nbm1;
-    const double2 lw = LW[j * nb + i];
+    const double2 lw = lds_d2(lw_s + (static_cast<std::uint32_t>(j) * nb + i) * C * 16u);  // lane's copy
     x[j] = __dadd_rn(lw.x, __dmul_rn(__dsub_rn(z, static_cast<double>(i)), lw.y));
     jac = __dmul_rn(jac, __dmul_rn(a.nbd, lw.y));
     bin[j] = i;
@@ -367,7 +415,10 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   // cells per axis: n_bins, plus one padding cell on the Philox path (see stage_grid_fast)
   const std::uint32_t nb = (NB ? static_cast<std::uint32_t>(NB) : a.nb) + (philox_stream(R) ? 1u : 0u);
   double2* LW = reinterpret_cast<double2*>(smem);
-  double* rcp = reinterpret_cast<double*>(LW + D * nb);
+  // grid-table copies (stage_grid): compile-time for the fixed-n_bins kernels
+  constexpr std::uint32_t kFixedC = NB ? fixed_tab_copies(D, static_cast<std::uint32_t>(NB) + (philox_stream(R) ? 1u : 0u)) : 0u;
+  const std::uint32_t C = kFixedC ? kFixedC : (a.tab_copies ? a.tab_copies : 1u);
+  double* rcp = reinterpret_cast<double*>(LW + D * nb * C);
   std::uint32_t* acc = reinterpret_cast<std::uint32_t*>(rcp + kRcpSmem);
   const int nacc = block_accs(a.bin_n, nb);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -383,13 +434,15 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     }
     pdl_wait();  // the grid, the stop flag and the exchange words come from the previous kernels
     if (a.stop && *a.stop) return;  // (uniform across the block)
-    if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
-    else stage_grid_fast<D>(LW, a);
+    if constexpr (R == RngKind::compat) stage_grid<D>(LW, a, C);
+    else stage_grid_fast<D>(LW, a, C);
   }
   __syncthreads();
   MCB_K1_STAMP(2, atomicMax)
 
   const int lane = tid & 31;
+  // this lane's table copy (stage_grid), as a 32-bit shared-window byte address
+  const std::uint32_t lw_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(LW)) + 16u * (static_cast<std::uint32_t>(lane) & (C - 1));
   std::uint32_t* bins = acc + kScalarAccs * kLaneCopies * kXWords;
   // 32-bit shared-window byte addresses of the accumulators
   const std::uint32_t acc_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(acc));
@@ -486,7 +539,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         double x[D];
         std::uint32_t bin[D];
         double fx;
-        const double fj = sample_point<F, D, NB>(a, f, LW, cd, croot, k, x, bin, fx);
+        const double fj = sample_point<F, D, NB>(a, f, lw_s, C, cd, croot, k, x, bin, fx);
         if (!isfinite(fj)) {  // sampler.hpp:170 -- the first failure in serial order is reported
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
           if (scalars) atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
@@ -512,7 +565,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         double x[D];
         std::uint32_t bin[D];
         double fx;
-        const double fj = sample_point_fast<F, D, NB>(a, f, LW, cw.dig, t, k, x, bin, fx);
+        const double fj = sample_point_fast<F, D, NB>(a, f, lw_s, C, cw.dig, t, k, x, bin, fx);
         if (!isfinite(fj)) {
           atomicMin(a.err_key, static_cast<unsigned long long>(t * a.p + k));
           if (scalars) atomicAdd(&nonfinite_s, 1u);  // exchanged with the words: all ranks stop together
@@ -521,10 +574,24 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         sum = __dadd_rn(sum, fj);
         // Welford with y = RN(1/n): mean += (f - mean) * y
         const std::uint32_t nk = k + 1;
+#if MCB_K1_RCPSEL
+        double y;
+        if (nk <= 2) y = nk == 1 ? 1.0 : 0.5;  // p = 2 (every BASELINE shape above 1e6 calls): no LDS
+        else y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
+#else
         const double y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
-        const double dd = __dsub_rn(fj, mean);
-        mean = __fma_rn(dd, y, mean);
-        m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
+#endif
+#if MCB_K1_PEEL
+        if (k == 0) {  // y = 1: the general update gives mean = fj, m2 = 0 (a zero's sign never reaches m2)
+          mean = fj;
+          m2 = 0.0;
+        } else
+#endif
+        {
+          const double dd = __dsub_rn(fj, mean);
+          mean = __fma_rn(dd, y, mean);
+          m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
+        }
         if (bin_n) deposit(fj, bin);
       }
       sum = __dmul_rn(sum, a.scale);
@@ -646,8 +713,8 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
                                     double* out_x, double* out_fx) {
   extern __shared__ __align__(16) unsigned char smem[];
   double2* LW = reinterpret_cast<double2*>(smem);
-  if constexpr (R == RngKind::compat) stage_grid<D>(LW, a);
-  else stage_grid_fast<D>(LW, a);
+  if constexpr (R == RngKind::compat) stage_grid<D>(LW, a, 1);
+  else stage_grid_fast<D>(LW, a, 1);
   __syncthreads();
   if (threadIdx.x != 0) return;
   double dg[D];
@@ -660,7 +727,7 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
   std::uint32_t bin[D];
   double fx;
   if constexpr (R == RngKind::compat) {
-    sample_point<F, D, 0>(a, f, LW, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
+    sample_point<F, D, 0>(a, f, static_cast<std::uint32_t>(__cvta_generic_to_shared(LW)), 1, dg, rng::feed(a.iter_root, t), static_cast<std::uint32_t>(k), x, bin, fx);
   } else {
     DigitT<D> dig[D];
     std::uint64_t t2 = t;
@@ -668,7 +735,7 @@ __global__ void sample_point_kernel(const SampleArgs a, const F f, std::uint64_t
       dig[j] = static_cast<DigitT<D>>(t2 % a.g);
       t2 /= a.g;
     }
-    sample_point_fast<F, D, 0>(a, f, LW, dig, t, static_cast<std::uint32_t>(k), x, bin, fx);
+    sample_point_fast<F, D, 0>(a, f, static_cast<std::uint32_t>(__cvta_generic_to_shared(LW)), 1, dig, t, static_cast<std::uint32_t>(k), x, bin, fx);
   }
   for (int j = 0; j < D; ++j) out_x[j] = x[j];
   *out_fx = fx;

@@ -60,7 +60,7 @@ static int graph_gain() {
   gpu::Run run(ctx, ops, cfg);
   cudaStream_t s = ctx.stream();
   auto body = [&] {
-    cudaMemsetAsync(ctx.state.get(), 0, sizeof(gpu::RunState), s);
+    cudaMemsetAsync(const_cast<int*>(run.stop_flag()) - offsetof(gpu::RunState, stop) / sizeof(int), 0, sizeof(gpu::RunState), s);
     for (std::uint32_t it = 1; it <= cfg.itmax; ++it) {
       run.sample(it);
       run.finish(it);

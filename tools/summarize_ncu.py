@@ -40,6 +40,15 @@ KEYS = [
     ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
      "GLOBAL reduction requests (only the per-block flush of nonzero exchange words; per-sample deposits stay in shared memory)"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smem atomic bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory data pipe busy % (one wavefront per clock per SM)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum.pct_of_peak_sustained_elapsed",
+     "  of which shared loads (grid table, reciprocals) %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum.pct_of_peak_sustained_elapsed",
+     "  of which shared atomics (exact deposits) %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "shared-load wavefronts"),
+    ("smsp__sass_inst_executed_op_shared_ld.sum", "shared-load warp instructions"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "shared-atomic wavefronts"),
     ("dram__bytes_read.sum", "DRAM bytes read"),
     ("dram__bytes_write.sum", "DRAM bytes written"),
 ]
