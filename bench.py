@@ -215,8 +215,8 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     dist = None
-    if world > 1:
-        import torch.distributed as dist_mod
+    import torch.distributed as dist_mod
+    if dist_mod.is_available() and dist_mod.is_initialized():  # N > 1, or MCB_FORCE_DIST=1 at N = 1
         dist = dist_mod
 
     ctx = M.Context(gpu)
@@ -727,7 +727,11 @@ def main():
         return run_suite(args.suite)
     if args.scale:
         return run_scale(args)
-    if world > 1:
+    # MCB_FORCE_DIST=1 runs the multi-rank code path (process group, exchange
+    # all-reduce, barriers, max over ranks) even at N = 1: on a one-GPU box
+    # that is the only way to exercise NCCL itself (tests/test_gpu_bench_dist.py)
+    use_dist = world > 1 or os.environ.get("MCB_FORCE_DIST") == "1"
+    if use_dist:
         import torch
         import torch.distributed as dist
 
@@ -743,7 +747,7 @@ def main():
     try:
         return run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
 
             dist.destroy_process_group()

@@ -79,12 +79,19 @@ __device__ __forceinline__ std::uint32_t atoms_add(std::uint32_t addr, std::uint
   return old;
 }
 
-/// Rare tail of a deposit: a carry out of the top word ripples upward.
+/// Rare tail of a deposit: a carry out of the top word ripples upward, at
+/// most to the accumulator's last word (`end` = one past it; a carry past it
+/// would need a sum beyond 2^1070, more than any block's deposits can reach).
+/// The bound is derived in this rare path from the deposit address and word
+/// index (acc_top), so the hot path keeps no extra live value.
 template <int kTag = 0>
 __device__ __noinline__ void carry_up_s(std::uint32_t addr, std::uint32_t end) {
   for (; addr < end; addr += 4)
     if (atoms_add(addr, 1u) != 0xffffffffu) break;
 }
+
+/// One past the last word of the accumulator whose word w sits at address a.
+__device__ __forceinline__ std::uint32_t acc_top(std::uint32_t a, std::uint32_t w) { return a + 4u * (kXWords - w); }
 
 /// Deposit the same digits into N accumulators (one per axis) -- the
 /// sampler's bin update, where every axis receives the same (f J)^2
@@ -95,7 +102,7 @@ __device__ __noinline__ void carry_up_s(std::uint32_t addr, std::uint32_t end) {
 /// with predicate carry-out / IADD3.X), and the rare ripple out of the top
 /// word is one check per sample.
 template <int N>
-__device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::uint32_t end, const Digits& dg) {
+__device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], const Digits& dg) {
   std::uint32_t t1[N], u[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
@@ -119,7 +126,7 @@ __device__ __forceinline__ void add_digits_s(const std::uint32_t (&a)[N], std::u
   if (ripple) {
 #pragma unroll
     for (int j = 0; j < N; ++j)
-      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(a[j] + 12, end);
+      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(a[j] + 12, acc_top(a[j], dg.w));
   }
 }
 
@@ -179,7 +186,7 @@ MCB_HD bool split_r24(double v, Digits2& out) {
 /// (= accumulator j + 4 dg.w): two word atomics (predicating the upper one
 /// off when its addend is zero measured slower), a rare ripple above.
 template <int N>
-__device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::uint32_t end, const Digits2& dg) {
+__device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], const Digits2& dg) {
   std::uint32_t t1[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
@@ -196,7 +203,7 @@ __device__ __forceinline__ void add_digits2_s(const std::uint32_t (&a)[N], std::
   if (ripple) {
 #pragma unroll
     for (int j = 0; j < N; ++j)
-      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a[j] + 8, 1u) == 0xffffffffu) carry_up_s(a[j] + 12, end);
+      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a[j] + 8, 1u) == 0xffffffffu) carry_up_s(a[j] + 12, acc_top(a[j], dg.w));
   }
 }
 #endif
@@ -216,8 +223,7 @@ __device__ __forceinline__ std::uint32_t atoms_add_at(std::uint32_t addr, std::u
 /// axis j's row offset j*kRow rides in the atomics' immediates, so a deposit
 /// costs one IMAD of address arithmetic per axis.
 template <int N, std::uint32_t kRow>
-__device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N], std::uint32_t end,
-                                                 const Digits2& dg) {
+__device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N], const Digits2& dg) {
   std::uint32_t t1[N];
   [&]<std::size_t... J>(std::index_sequence<J...>) {
     ((void)[&] {
@@ -237,7 +243,7 @@ __device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N],
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const std::uint32_t a = base[j] + static_cast<std::uint32_t>(j) * kRow;
-      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a + 8, 1u) == 0xffffffffu) carry_up_s(a + 12, end);
+      if ((ripple >> (N - 1 - j)) & 1u && atoms_add(a + 8, 1u) == 0xffffffffu) carry_up_s(a + 12, acc_top(a, dg.w));
     }
   }
 }
@@ -247,8 +253,7 @@ __device__ __forceinline__ void add_digits2_rows(const std::uint32_t (&base)[N],
 /// add_digits_s (three words, the exact addend) with the axis row offsets
 /// j*kRow as immediates, as add_digits2_rows: the Philox stream with exact bins.
 template <int N, std::uint32_t kRow>
-__device__ __forceinline__ void add_digits_rows(const std::uint32_t (&base)[N], std::uint32_t end,
-                                                const Digits& dg) {
+__device__ __forceinline__ void add_digits_rows(const std::uint32_t (&base)[N], const Digits& dg) {
   std::uint32_t t1[N], u[N];
   [&]<std::size_t... J>(std::index_sequence<J...>) {
     ((void)[&] {
@@ -276,7 +281,10 @@ __device__ __forceinline__ void add_digits_rows(const std::uint32_t (&base)[N], 
   if (ripple) {
 #pragma unroll
     for (int j = 0; j < N; ++j)
-      if ((ripple >> (N - 1 - j)) & 1u) carry_up_s(base[j] + static_cast<std::uint32_t>(j) * kRow + 12, end);
+      if ((ripple >> (N - 1 - j)) & 1u) {
+        const std::uint32_t a = base[j] + static_cast<std::uint32_t>(j) * kRow;
+        carry_up_s(a + 12, acc_top(a, dg.w));
+      }
   }
 }
 #endif
@@ -284,8 +292,7 @@ __device__ __forceinline__ void add_digits_rows(const std::uint32_t (&base)[N], 
 /// Two independent exact adds (the per-cube estimate and variance) at
 /// shared-window addresses a_s / b_s (accumulator bases), issued interleaved
 /// so their atomic round trips overlap.
-__device__ __forceinline__ void add_shared2_s(std::uint32_t a_s, double a, std::uint32_t b_s, double b,
-                                              std::uint32_t end_s) {
+__device__ __forceinline__ void add_shared2_s(std::uint32_t a_s, double a, std::uint32_t b_s, double b) {
   Digits da, db;
   const bool ha = split(a, da), hb = split(b, db);
   if (ha && hb) {
@@ -308,15 +315,15 @@ __device__ __forceinline__ void add_shared2_s(std::uint32_t a_s, double a, std::
     o = atoms_add(pb + 8, tb);
     asm("{\n\t.reg .u32 z;\n\tadd.cc.u32 z, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t}" : "=r"(rb) : "r"(o), "r"(tb));
     if (ra | rb) {
-      if (ra) carry_up_s(pa + 12, end_s);
-      if (rb) carry_up_s(pb + 12, end_s);
+      if (ra) carry_up_s(pa + 12, acc_top(pa, da.w));
+      if (rb) carry_up_s(pb + 12, acc_top(pb, db.w));
     }
   } else if (ha) {
     const std::uint32_t pa[1] = {a_s + 4u * da.w};
-    add_digits_s<1>(pa, end_s, da);
+    add_digits_s<1>(pa, da);
   } else if (hb) {
     const std::uint32_t pb[1] = {b_s + 4u * db.w};
-    add_digits_s<1>(pb, end_s, db);
+    add_digits_s<1>(pb, db);
   }
 }
 

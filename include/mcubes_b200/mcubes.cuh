@@ -42,6 +42,9 @@
 #include <vector>
 
 #include "engine.cuh"
+#if MCB_NVTX
+#include <nvtx3/nvToolsExt.h>
+#endif
 
 namespace mcubes {
 
@@ -118,6 +121,27 @@ struct EstimateVariance {
 };
 
 namespace gpu {
+
+/// NVTX range for profilers (nsys / ncu --nvtx): the whole integrate() and
+/// each enqueued iteration.  No-ops unless a tool is attached; MCB_NVTX=0 at
+/// build time removes them.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+#if MCB_NVTX
+    nvtxRangePushA(name);
+#else
+    (void)name;
+#endif
+  }
+  ~NvtxRange() {
+#if MCB_NVTX
+    nvtxRangePop();
+#endif
+  }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 /// One context per (host thread, device), created on first use.
 inline Context& default_context() {
@@ -960,6 +984,7 @@ class Run {
 inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, const RunConfig& cfg,
                                        const IterationObserver& observe = {}, const Grid* resume_grid = nullptr,
                                        std::span<const IterationResult> resume_history = {}) {
+  const NvtxRange whole("mcubes::integrate");
   Run run(ctx, ops, cfg);
   const std::uint32_t first = resume_grid ? run.resume(*resume_grid, resume_history) : 1u;
   if (first > 1 && run.state().stop) return run.result();  // the checkpoint had already converged
@@ -982,9 +1007,12 @@ inline IntegrationResult integrate_ops(Context& ctx, const IntegrandOps& ops, co
       MCB_CUDA(cudaEventSynchronize(ctx.event(back % (kAhead + 1))));
       if (reinterpret_cast<volatile int*>(flags)[back - 1] != 1) break;  // stopped (or never ran: stopped earlier)
     }
-    run.sample(it);
-    run.reduce(it);
-    run.finish(it);
+    {
+      const NvtxRange r(it <= cfg.ita ? "mcubes::iteration (adjusting)" : "mcubes::iteration (frozen)");
+      run.sample(it);
+      run.reduce(it);
+      run.finish(it);
+    }
     if (lookahead) MCB_CUDA(cudaEventRecord(ctx.event(it % (kAhead + 1)), ctx.stream()));
     if (observe) {
       const RunState st = run.state();

@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
   const std::uint32_t est_neg_s = acc_s + (1 * kLaneCopies + lane) * kAccBytes;
   const std::uint32_t var_s = acc_s + (2 * kLaneCopies + lane) * kAccBytes;
   const std::uint32_t bins_s = acc_s + kScalarAccs * kLaneCopies * kAccBytes;
-  const std::uint32_t end_s = acc_s + static_cast<std::uint32_t>(nacc) * kAccBytes;
   // The compile-time-n_bins kernels (NB != 0) run every shape in one pass
   // (launch_k1 sends multi-pass shapes to NB = 0), so their pass logic folds away.
   constexpr bool kOnePass = NB != 0;
@@ -487,27 +486,27 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
           std::uint32_t base[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) base[j] = wb + bin[j] * kCell;
-          if constexpr (kR24) exact::add_digits2_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
-          else exact::add_digits_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, end_s, dgt);
+          if constexpr (kR24) exact::add_digits2_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, dgt);
+          else exact::add_digits_rows<D, static_cast<std::uint32_t>(NB + 1) * kCell>(base, dgt);
         } else {
           std::uint32_t ad[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) ad[j] = wb + bin[j] * kCell + static_cast<std::uint32_t>(j) * nb * kCell;
-          if constexpr (kR24) exact::add_digits2_s<D>(ad, end_s, dgt);
-          else exact::add_digits_s<D>(ad, end_s, dgt);
+          if constexpr (kR24) exact::add_digits2_s<D>(ad, dgt);
+          else exact::add_digits_s<D>(ad, dgt);
         }
       } else if (kOnePass || (bin_n == 1 && bin_lo == 0)) {  // BinUpdate::axis0_only
         const std::uint32_t ad[1] = {wb + bin[0] * kCell};
-        if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
-        else exact::add_digits_s<1>(ad, end_s, dgt);
+        if constexpr (kR24) exact::add_digits2_s<1>(ad, dgt);
+        else exact::add_digits_s<1>(ad, dgt);
       } else {  // a pass over axes [bin_lo, bin_lo + bin_n) (compile-time axis index, runtime predicate)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const std::uint32_t rel = static_cast<std::uint32_t>(j) - bin_lo;
           if (rel < bin_n) {
             const std::uint32_t ad[1] = {wb + bin[j] * kCell + rel * nb * kCell};
-            if constexpr (kR24) exact::add_digits2_s<1>(ad, end_s, dgt);
-            else exact::add_digits_s<1>(ad, end_s, dgt);
+            if constexpr (kR24) exact::add_digits2_s<1>(ad, dgt);
+            else exact::add_digits_s<1>(ad, dgt);
           }
         }
       }
@@ -600,7 +599,7 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     if (!(var > 0.0)) var = 0.0;  // sampler.hpp:179 (a NaN variance becomes 0, an infinite one stays)
     if (scalars) {
       ovf |= !(fabs(sum) < INFINITY) || !(var < INFINITY);  // ExactSum::add would throw (exact_sum.hpp:34)
-      exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var, end_s);
+      exact::add_shared2_s(sum < 0.0 ? est_neg_s : est_pos_s, sum, var_s, var);
     }
 
     bool all_axes;

@@ -36,16 +36,17 @@ namespace gpu::fn {
 struct Suite {
   int family = 0;
   double norm = 0.0;
+  ExpConsts ec;  ///< exp's constants, carried in the kernel parameters (integrands.cuh)
   MCB_HD double operator()(std::span<const double> x) const {
     switch (family) {
       case 1: return F1{}(x);
       case 2: return F2{}(x);
       case 3: return F3{}(x);
-      case 4: return F4{}(x);
-      case 5: return F5{}(x);
-      case 6: return F6{}(x);
+      case 4: return F4{ec}(x);
+      case 5: return F5{ec}(x);
+      case 6: return F6{ec}(x);
       case 7: return FA{}(x);
-      default: return FB{norm}(x);
+      default: return FB{norm, ec}(x);
     }
   }
 };

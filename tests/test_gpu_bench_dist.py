@@ -54,3 +54,20 @@ def test_bench_world4_matches_single_gpu(transport):
     for k in ("estimate", "sigma", "chi2_dof", "samples", "bin_writes"):
         assert four["result"][k] == one["result"][k], k
     assert four["result"]["samples"] == (3 + 2) * one["config"]["evals_per_step"]
+
+
+def test_bench_nccl_path_world1_matches_single_gpu():
+    """The N > 1 code path over NCCL itself (process group bound to the
+    device, the exact int64 exchange all-reduced by NCCL on the library's
+    stream, barriers, max over ranks), run at world 1 with MCB_FORCE_DIST=1:
+    NCCL cannot put two ranks on one GPU, and this box has one."""
+    one = _bench(1)
+    env = dict(os.environ, MCB_FORCE_DIST="1")
+    env.pop("MCB_DIST_BACKEND", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", *ARGS]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    nccl = _line(p.stdout)
+    for k in ("estimate", "sigma", "chi2_dof", "samples", "bin_writes"):
+        assert nccl["result"][k] == one["result"][k], k
