@@ -17,6 +17,14 @@ for rng in ("compat", "philox"):
         M.v_sample_no_adjust(f, g, m, 1, 2, 1, 2, rng=rng, ctx=ctx)
     cfg = M.RunConfig(dims=4, maxcalls=20000, itmax=4, ita=2, tau_rel=1e-12, lower=[0.0] * 4, upper=[1.0] * 4, rng=rng)
     M.integrate(M.make_suite_integrand(4, 4), cfg, ctx=ctx)
+    # runtime n_bins (grid-table copies chosen at launch) and bin passes
+    # (8D at 200 bins: the histograms of all axes exceed one CTA)
+    for d, nb, m in ((3, 100, 12 ** 3), (8, 200, 2 ** 8)):
+        g = M.Grid(d, nb, [0.0] * d, [1.0] * d)
+        M.v_sample(M.make_suite_integrand(4, d), g, m, 1, 3, 1, 1, rng=rng, ctx=ctx)
+# Philox with exact bins
+g = M.Grid(5, 50, [0.0] * 5, [1.0] * 5)
+M.v_sample(M.make_suite_integrand(4, 5), g, 5 ** 5, 1, 2, 1, 1, rng="philox", bins="exact", ctx=ctx)
 # the peer-memory exchange (two virtual ranks on this GPU, phases separated by device syncs)
 import ctypes as C  # noqa: E402
 
