@@ -225,6 +225,10 @@ def run_ours(args, rank, world, local_rank):
     # --transport peer (N > 1): K1 writes every rank's exchange buffer over
     # peer memory and no collective runs in the step (one PeerExchange per run)
     peer = dist is not None and args.transport == "peer"
+    # --transport compact (N > 1): every rank rounds its slice, the ranks
+    # all-gather d x n_bins + 6 doubles and sum them in rank order (dist.py)
+    compact = dist is not None and args.transport == "compact"
+    cbufs = {}
     exchanges = []
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -247,8 +251,27 @@ def run_ours(args, rank, world, local_rank):
             px = PeerExchange(ctx, run.exchange_words())
             px.attach(run)
             exchanges.append(px)
+        if compact:
+            cl = run.compact_len()
+            cbufs[id(run)] = (torch.zeros(cl, dtype=torch.float64, device=dev),
+                              torch.zeros(world * cl, dtype=torch.float64, device=dev))
         m = run.work_items
         return run, xbuf, m, rank * m // world, (rank + 1) * m // world
+
+    def exchange_finish(run, xbuf, it):
+        """The step's exchange and finish: exact all-reduce (collective), none
+        (peer: K1 already wrote every rank's buffer) or the compact all-gather."""
+        if compact:
+            from paper_2202_01753_b200.dist import all_gather_rank_major
+            mine, every = cbufs[id(run)]
+            run.round_local(it, mine.data_ptr())
+            all_gather_rank_major(every, mine)
+            run.combine(it, every.data_ptr(), world)
+            run.finish_rounded(it)
+            return
+        if dist is not None and not peer:
+            dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
+        run.finish(it)
 
     def measure(maxcalls, rng, bins, steps, warmup, seed=0, clocks=None):
         """W warm-up + K timed adjusting steps of one run: the grid starts
@@ -263,9 +286,7 @@ def run_ours(args, rank, world, local_rank):
             if k1_events:
                 k1_events[1].record(stream)
             run.reduce(it)
-            if dist is not None and not peer:
-                dist.all_reduce(xbuf)  # exact: integer digit sums (MCB_XWORDS words per accumulator)
-            run.finish(it)
+            exchange_finish(run, xbuf, it)
 
         for it in range(1, warmup + 1):
             step(it)
@@ -321,9 +342,7 @@ def run_ours(args, rank, world, local_rank):
         run2.set_grid(host_edges)                # H2D: the step's input grid
         run2.sample(it, n0, n1)
         run2.reduce(it)
-        if dist is not None and not peer:
-            dist.all_reduce(xbuf2)
-        run2.finish(it)
+        exchange_finish(run2, xbuf2, it)
         run2.grid_into(out_edges)                # D2H: adapted grid (synchronises)
         host_edges[:] = out_edges                # the next step samples on it
 
@@ -373,6 +392,7 @@ def run_ours(args, rank, world, local_rank):
         "reductions": BINS_DESC[args.bins if args.rng == "philox" else "exact"],
         "parallelism": ((f"cube-range partition x{world} + " +
                          ("exact exchange over peer memory inside K1" if peer
+                          else f"compact all-gather of rounded partials ({dist.get_backend()})" if compact
                           else f"exact all-reduce ({dist.get_backend()})")) if world > 1 else "single GPU"),
         "clocks": head["clocks"],
         "gpu_launches": head["launches"],
@@ -416,7 +436,7 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu_baseline(args.maxcalls)
         line["time_to_epsrel"] = time_to_epsrel(M, ctx)
     elif world > 1 and not args.no_cpu:
-        tte = time_to_epsrel_dist(M, ctx, dist, dev, rank, "peer" if peer else "collective")
+        tte = time_to_epsrel_dist(M, ctx, dist, dev, rank, args.transport)
         if rank == 0:
             line["time_to_epsrel"] = tte
     if rank == 0:
@@ -701,9 +721,11 @@ def main():
                     help="philox: contribution addends rounded to 24 significant bits (headline) or exact")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the secondary lines (exact bins, compat stream, maxcalls 1e10)")
-    ap.add_argument("--transport", choices=["collective", "peer"], default="collective",
-                    help="N > 1: exchange through an NCCL all-reduce, or K1 writing every rank's buffer over "
-                         "peer memory (CUDA IPC over NVLink)")
+    ap.add_argument("--transport", choices=["collective", "peer", "compact"], default="collective",
+                    help="N > 1: exchange through an exact NCCL all-reduce (216 KB at 8D, results independent of "
+                         "N), K1 writing every rank's buffer over peer memory (CUDA IPC over NVLink), or the compact "
+                         "all-gather of each rank's rounded d*n_bins+6 doubles (3.2 KB per rank, N-dependent last "
+                         "bits)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / time_to_epsrel legs")
     ap.add_argument("--suite", default=None, help="run BASELINE configs 1-5 (GPU + reference CPU) into this JSONL")
     ap.add_argument("--scale", default=None,

@@ -270,6 +270,23 @@ int mcb_run_sample(mcb_run* run, uint32_t it, uint64_t n0, uint64_t n1);
 int mcb_run_reduce(mcb_run* run, uint32_t it);
 /* K3b + K4: round, adapt the grid, combine, convergence gate. */
 int mcb_run_finish(mcb_run* run, uint32_t it);
+
+/* ---- compact exchange: SURVEY.md section 8(e)'s all-gather of each rank's
+ * rounded (d*n_bins + 2) doubles, combined in a fixed rank order (replaces
+ * the reference's in-process merge of worker partials, sampler.hpp:272-276,
+ * across GPUs).  Per iteration: mcb_run_sample on the rank's slice;
+ * mcb_run_round_local into a device buffer of mcb_run_compact_len(run)
+ * doubles (estimate, variance, 4 u64 counts bit-cast to doubles --
+ * samples, writes, overflowed addends, non-finite samples -- then the
+ * contributions); all-gather those buffers rank-major; mcb_run_combine sums
+ * them in rank order on the device; mcb_run_finish_rounded adapts the grid
+ * and updates the weighted estimate (driver.hpp:231-252).  Every rank holds
+ * identical state; the last bits depend on the rank count (each rank rounds
+ * its partial sums), one rank is bitwise the exact path. */
+uint64_t mcb_run_compact_len(const mcb_run* run);
+int mcb_run_round_local(mcb_run* run, uint32_t it, double* out);
+int mcb_run_combine(mcb_run* run, uint32_t it, const double* gathered, int nranks);
+int mcb_run_finish_rounded(mcb_run* run, uint32_t it);
 int mcb_run_result(mcb_run* run, mcb_result* result, mcb_iteration* history, uint32_t history_cap);
 /* Replace the device grid with host edges (dims*n_bins); stream-ordered. */
 int mcb_run_set_grid(mcb_run* run, const double* edges);

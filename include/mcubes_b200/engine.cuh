@@ -563,7 +563,7 @@ inline int adjust_warps(std::uint32_t dims, std::uint32_t nb, int max_smem) {
 /// an epilogue, also grid adaptation + weighted estimate + convergence.
 inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes, unsigned long long* words,
                           double* est, double* var, double* contrib, const int* stop, const EpilogueArgs* epi,
-                          bool zero_words = false, unsigned long long* counts = nullptr) {
+                          bool zero_words = false, unsigned long long* counts = nullptr, bool prerounded = false) {
   RoundArgs r{};
   r.words = words;
   r.dims = sh.dims;
@@ -575,7 +575,8 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   r.contrib = contrib;
   r.counts = counts;
   r.stop = stop;
-  r.zero_words = (zero_words && epi) ? 1 : 0;
+  r.zero_words = zero_words ? 1 : 0;
+  r.prerounded = prerounded ? 1 : 0;
   if (epi && ctx.peer.npeers) {
     r.wait_flags = ctx.peer.my_flags;
     r.nwait = ctx.peer.npeers;
@@ -605,8 +606,8 @@ inline void launch_finish(Context& ctx, const Shape& sh, std::uint32_t bin_axes,
   }
   const int values = static_cast<int>(sh.dims * sh.nb + 2);  // one warp per output value
   const int warps_per_block = kFinishThreads / 32;
-  launch_pdl(finish_kernel<0>, (values + warps_per_block - 1) / warps_per_block, kFinishThreads, smem, ctx.stream(), r,
-             e, epi ? 1 : 0, counter);
+  const int blocks = prerounded ? 1 : (values + warps_per_block - 1) / warps_per_block;  // prerounded: epilogue only
+  launch_pdl(finish_kernel<0>, blocks, kFinishThreads, smem, ctx.stream(), r, e, epi ? 1 : 0, counter);
   ++ctx.launches;
 }
 

@@ -488,9 +488,14 @@ struct RoundArgs {
   double* est;       ///< 1 double
   double* var;       ///< 1 double
   double* contrib;   ///< dims*nb (nullable: frozen iterations keep only shared copies)
-  unsigned long long* counts;  ///< nullable: {samples, writes, overflowed addends} of this iteration (no epilogue)
+  unsigned long long* counts;  ///< nullable: {samples, writes, overflowed addends, non-finite samples} of this
+                               ///< iteration (no epilogue)
   const int* stop;
-  int zero_words;  ///< epilogue leaves the exchange words zeroed for the next K1 flush (integrate loop)
+  int zero_words;  ///< leave the exchange words zeroed for the next K1 flush (integrate loop, compact exchange)
+  /// The estimate, variance, contributions and header counts are already in
+  /// place (the compact exchange combined every rank's rounded values,
+  /// Run::combine): skip the rounding, run the epilogue only.
+  int prerounded;
   const unsigned long long* wait_flags;  ///< peer-memory exchange: wait until these nwait flags reach wait_value
   int nwait;
   unsigned long long wait_value;
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
     for (int w = lane; w < naccs * kXWords; w += 32) w0[w] = 0ull;
   };
   const int c = blockIdx.x * nwarps + warp;
-  if (c < total + 2) {
+  if (!r.prerounded && c < total + 2) {
     if (c == total) {
       const double v = exact::warp_round_words(r.words, r.words + kXWords);
       if (lane == 0) *r.est = v;
@@ -571,6 +576,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
       r.counts[0] = r.words[-2];
       r.counts[1] = r.words[-2] * r.bin_axes;
       r.counts[2] = r.words[-3];
+      r.counts[3] = r.words[-1];
+      if (r.zero_words) r.words[-1] = r.words[-2] = r.words[-3] = 0ull;
     }
     return;
   }
@@ -647,6 +654,45 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(const RoundArgs 
   else if (e.adjusting) adjust_grid_block(e.adj, contrib_s, edges_s, scratch, e.adj_warps);
   if (threadIdx.x == 0) MCB_FIN_STAMP(4);
   if (!concurrent && warp == 0) estimate();
+}
+
+// ------------------------------------------------------------------ compact exchange
+/// Layout of one rank's rounded iteration in the compact exchange
+/// (Run::round_local): estimate, variance (already / m^2), then four u64
+/// counts stored bit for bit in doubles -- finite samples, writes, overflowed
+/// addends, non-finite samples -- then the d x n_bins contributions.
+inline constexpr int kCompactHead = 6;
+
+/// Combine the G ranks' rounded iterations (gathered[r * len + i], the
+/// layout above) in rank order -- sum = v_0 + v_1 + ... + v_{G-1}, the same
+/// sequence of IEEE additions on every rank, so every rank holds identical
+/// values -- into the run's history slot, contributions and exchange header
+/// (the counts the epilogue reads).  SURVEY.md section 8(e)'s all-gather of
+/// d x n_bins + 2 doubles, combined in a fixed order.
+template <int kTag = 0>
+__global__ void combine_kernel(const double* __restrict__ gathered, int nranks, int len, int ncontrib,
+                               double* est, double* var, double* contrib, unsigned long long* header,
+                               const int* stop) {
+  pdl_trigger();
+  pdl_wait();
+  if (*stop) return;  // the run has finished; later iterations are no-ops
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    if (i >= 2 && i < kCompactHead) {  // counts: exact integer sums
+      unsigned long long c = 0;
+      for (int q = 0; q < nranks; ++q)
+        c += static_cast<unsigned long long>(__double_as_longlong(gathered[static_cast<std::size_t>(q) * len + i]));
+      if (i == 2) header[1] = c;  // finite samples   (words[-2])
+      if (i == 4) header[0] = c;  // overflowed addends (words[-3])
+      if (i == 5) header[2] = c;  // non-finite samples (words[-1])
+      continue;
+    }
+    if (i >= kCompactHead && i - kCompactHead >= ncontrib) continue;  // frozen iteration: no contributions
+    double acc = gathered[i];
+    for (int q = 1; q < nranks; ++q) acc = __dadd_rn(acc, gathered[static_cast<std::size_t>(q) * len + i]);
+    if (i == 0) *est = acc;
+    else if (i == 1) *var = acc;
+    else contrib[i - kCompactHead] = acc;
+  }
 }
 
 // ------------------------------------------------------------------ run setup / collect

@@ -103,6 +103,10 @@ SIGNATURES = {
     "mcb_run_sample": (C.c_int, [_VP, _U32, _U64, _U64]),
     "mcb_run_reduce": (C.c_int, [_VP, _U32]),
     "mcb_run_finish": (C.c_int, [_VP, _U32]),
+    "mcb_run_compact_len": (_U64, [_VP]),
+    "mcb_run_round_local": (C.c_int, [_VP, _U32, _VP]),
+    "mcb_run_combine": (C.c_int, [_VP, _U32, _VP, C.c_int]),
+    "mcb_run_finish_rounded": (C.c_int, [_VP, _U32]),
     "mcb_run_result": (C.c_int, [_VP, C.POINTER(mcb_result), C.POINTER(mcb_iteration), _U32]),
     "mcb_run_set_grid": (C.c_int, [_VP, _PD]),
     "mcb_run_grid": (C.c_int, [_VP, _PD]),

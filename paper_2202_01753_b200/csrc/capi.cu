@@ -496,6 +496,32 @@ int mcb_run_finish(mcb_run* r, uint32_t it) {
   });
 }
 
+uint64_t mcb_run_compact_len(const mcb_run* r) { return r ? r->run->compact_len() : 0; }
+
+int mcb_run_round_local(mcb_run* r, uint32_t it, double* out) {
+  if (!r || !out) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    if (it < 1 || it > r->cfg.itmax) throw std::invalid_argument("iteration out of range");
+    r->run->round_local(it, out);
+  });
+}
+
+int mcb_run_combine(mcb_run* r, uint32_t it, const double* gathered, int nranks) {
+  if (!r || !gathered) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    if (it < 1 || it > r->cfg.itmax) throw std::invalid_argument("iteration out of range");
+    r->run->combine(it, gathered, nranks);
+  });
+}
+
+int mcb_run_finish_rounded(mcb_run* r, uint32_t it) {
+  if (!r) return MCB_EINVAL;
+  return guarded(r->owner, [&] {
+    if (it < 1 || it > r->cfg.itmax) throw std::invalid_argument("iteration out of range");
+    r->run->finish_rounded(it);
+  });
+}
+
 int mcb_run_result(mcb_run* r, mcb_result* result, mcb_iteration* history, uint32_t cap) {
   if (!r) return MCB_EINVAL;
   return guarded(r->owner, [&] { fill_result(r->run->result(), result, history, cap); });

@@ -12,6 +12,13 @@ equal to the single-GPU (and reference) result.  This replaces the
 reference's in-process exact merge of per-worker partials
 (sampler.hpp:272-276).
 
+transport="compact" is SURVEY.md section 8(e)'s exchange: every rank rounds
+its own slice to d x n_bins + 2 doubles (plus the counts), the ranks
+all-gather them (3.2 KB per rank at 8D instead of 216 KB), and every rank
+sums them in rank order on the device and runs the epilogue: identical state
+on every rank, last bits dependent on the GPU count (one rank is bitwise the
+exact path).
+
 transport="peer" replaces the all-reduce by the sampling kernel itself:
 its blocks add their words into every rank's buffer over peer memory (CUDA
 IPC mappings, system-scope reductions) and release a per-iteration flag that
@@ -22,6 +29,17 @@ from __future__ import annotations
 from typing import Optional
 
 from . import mcubes as M
+
+
+def all_gather_rank_major(every, mine, group=None):
+    """every[r * len(mine):(r + 1) * len(mine)] = rank r's `mine` (NCCL: one
+    all_gather_into_tensor; gloo, which lacks it: the list form)."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(every, mine, group=group)
+    else:
+        dist.all_gather(list(every.view(-1, mine.numel()).unbind(0)), mine, group=group)
 
 
 def partition(m: int, world: int, rank: int):
@@ -134,8 +152,8 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
     transport="peer" has K1 write every rank's buffer directly over peer
     memory (CUDA IPC, system-scope reductions and flags), with no collective
     inside the iteration loop."""
-    if transport not in ("collective", "peer"):
-        raise ValueError("transport must be 'collective' or 'peer'")
+    if transport not in ("collective", "peer", "compact"):
+        raise ValueError("transport must be 'collective', 'peer' or 'compact'")
     import torch
     import torch.distributed as dist
 
@@ -167,6 +185,9 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
             else:
                 xbuf = torch.zeros(run.exchange_words(), dtype=torch.int64, device=dev)
                 run.set_exchange(xbuf.data_ptr())
+            if transport == "compact":
+                mine = torch.zeros(run.compact_len(), dtype=torch.float64, device=dev)
+                every = torch.zeros(world * run.compact_len(), dtype=torch.float64, device=dev)
             first = run.resume(resume) if resume is not None else 1
             if first > 1 and run.result().converged:
                 return run.result()
@@ -177,11 +198,17 @@ def integrate(f: M.IntegrandSpec, cfg: M.RunConfig, group=None, ctx: Optional[M.
                         break
                 run.sample(it, n0, n1)
                 run.reduce(it)
-                if peers is None:
-                    # exact integer sum across ranks, of the words this iteration uses
-                    # (frozen iterations: the count words and est+/est-/var only)
-                    dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
-                run.finish(it)
+                if transport == "compact":
+                    run.round_local(it, mine.data_ptr())
+                    all_gather_rank_major(every, mine, group)
+                    run.combine(it, every.data_ptr(), world)
+                    run.finish_rounded(it)
+                else:
+                    if peers is None:
+                        # exact integer sum across ranks, of the words this iteration uses
+                        # (frozen iterations: the count words and est+/est-/var only)
+                        dist.all_reduce(xbuf[:run.exchange_words(it)], group=group)
+                    run.finish(it)
                 events[it % (ahead + 1)].record(stream)
                 if observer is not None:
                     # a failed iteration stops here, before result() (which raises): the

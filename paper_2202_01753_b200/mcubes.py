@@ -876,6 +876,22 @@ class Run:
     def finish(self, it: int):
         _raise(self._lib.mcb_run_finish(self.ptr, it), self.ctx.ptr, self.cfg.dims)
 
+    # compact exchange (include/mcubes_b200.h): round this rank's slice,
+    # all-gather, combine in rank order, epilogue
+    def compact_len(self) -> int:
+        """Doubles per rank in the compact exchange (d * n_bins + 6)."""
+        return int(self._lib.mcb_run_compact_len(self.ptr))
+
+    def round_local(self, it: int, device_ptr: int):
+        _raise(self._lib.mcb_run_round_local(self.ptr, it, C.c_void_p(device_ptr)), self.ctx.ptr, self.cfg.dims)
+
+    def combine(self, it: int, gathered_ptr: int, nranks: int):
+        _raise(self._lib.mcb_run_combine(self.ptr, it, C.c_void_p(gathered_ptr), nranks), self.ctx.ptr,
+               self.cfg.dims)
+
+    def finish_rounded(self, it: int):
+        _raise(self._lib.mcb_run_finish_rounded(self.ptr, it), self.ctx.ptr, self.cfg.dims)
+
     def step(self, it: int):
         """One whole iteration on this device (sample, reduce, finish)."""
         self.sample(it)

@@ -176,3 +176,65 @@ def test_peer_exchange_host_tables():
         assert opened == closed and len(opened) == 3 * (world - 1)
         assert all(p // 1000 != rank + 1 for p in opened)
         assert sorted(e[1] for e in log if e[0] == "free") == sorted(a[1] for a in allocs)
+
+
+def _compact_rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        from paper_2202_01753_b200.dist import all_gather_rank_major, partition
+
+        # each rank's rounded slice in the compact layout (est, var, 4 counts, contributions)
+        d, nb, fam, p, seed, g = 3, 10, 2, 3, 5, 7
+        m = g ** d
+        lo, hi = [0.0] * d, [1.0] * d
+        edges = O.uniform_edges(d, nb, lo, hi)
+        n0, n1 = partition(m, world, rank)
+        words = np.zeros((3 + d * nb) * O.XWORDS, dtype=np.uint64)
+        assert O.orc().orc_sample_partial(fam, None, 0, d, nb, O.darr(lo), O.darr(hi), O.ptr(edges), m, p, seed, 1,
+                                          0, 1, n0, n1, words.ctypes.data_as(C.POINTER(C.c_uint64)), None, None,
+                                          None) == 0
+        est, var = C.c_double(), C.c_double()
+        contrib = np.zeros(d * nb)
+        O.orc().orc_round_partial(words.ctypes.data_as(C.POINTER(C.c_uint64)), d, nb, m, 0, 1, C.byref(est),
+                                  C.byref(var), O.ptr(contrib))
+        counts = np.array([(n1 - n0) * p, (n1 - n0) * p * d, 0, 0], dtype=np.uint64).view(np.float64)
+        mine = torch.from_numpy(np.concatenate([[est.value, var.value], counts, contrib]))
+        every = torch.zeros(world * mine.numel(), dtype=torch.float64)
+        all_gather_rank_major(every, mine)
+        q.put((rank, mine.numpy().tobytes(), every.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_compact_exchange_gathers_rank_major():
+    """dist.all_gather_rank_major (transport='compact') over gloo, world 3:
+    every rank receives every rank's rounded slice at offset rank * len, and
+    the combine that Run.combine performs on the device -- the per-rank values
+    added in rank order -- gives one result on every rank, within the partial
+    sums' rounding of the single-process iteration."""
+    import oracle as O
+
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_compact_rank, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    mines = [np.frombuffer(r[1], dtype=np.float64) for r in res]
+    for _, _, ev in res:
+        assert np.array_equal(np.frombuffer(ev, dtype=np.float64).view(np.uint64),
+                              np.concatenate(mines).view(np.uint64))
+    est = mines[0][0]
+    for r in range(1, world):
+        est = est + mines[r][0]
+    d, nb = 3, 10
+    want = O.v_sample("orc", 2, None, d, nb, [0.0] * d, [1.0] * d, None, 7 ** d, 1, 3, 5, 1)
+    assert abs(est - want["est"]) <= 1e-14 * abs(want["est"])
+    assert sum(int(m_[2:6].view(np.uint64)[0]) for m_ in mines) == want["writes"] // d

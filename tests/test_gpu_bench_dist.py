@@ -71,3 +71,16 @@ def test_bench_nccl_path_world1_matches_single_gpu():
     nccl = _line(p.stdout)
     for k in ("estimate", "sigma", "chi2_dof", "samples", "bin_writes"):
         assert nccl["result"][k] == one["result"][k], k
+
+
+def test_bench_world4_compact_exchange():
+    """--transport compact (SURVEY.md 8(e)'s all-gather of each rank's
+    rounded d*n_bins+6 doubles, summed in rank order): the same samples as
+    one GPU and estimates within the rounding of the per-rank partial sums."""
+    one = _bench(1)
+    four = _bench(4, "compact")
+    assert four["n_gpus"] == 4 and "compact" in four["parallelism"]
+    assert four["result"]["samples"] == one["result"]["samples"]
+    assert four["result"]["bin_writes"] == one["result"]["bin_writes"]
+    assert abs(four["result"]["estimate"] - one["result"]["estimate"]) <= 1e-12 * abs(one["result"]["estimate"])
+    assert abs(four["result"]["sigma"] - one["result"]["sigma"]) <= 1e-10 * one["result"]["sigma"]

@@ -174,6 +174,67 @@ def test_simulated_ranks_equal_single_gpu(ctx):
         ctx.set_stream(0)
 
 
+def _compact_run(f, cfg, ctx, G, stream):
+    """The compact exchange with G simulated ranks on one GPU: each rank's
+    slice is sampled and rounded on its own (round_local), the rank-major
+    buffer is what the all-gather delivers, then combine + finish_rounded.
+    Returns the result and every iteration's gathered buffer."""
+    gathered = []
+    with torch.cuda.stream(stream):
+        run = M.Run(f, cfg, ctx)
+        m, L = run.work_items, run.compact_len()
+        every = torch.zeros(G * L, dtype=torch.float64, device="cuda")
+        for it in range(1, cfg.itmax + 1):
+            for r in range(G):
+                run.sample(it, r * m // G, (r + 1) * m // G)
+                run.reduce(it)
+                run.round_local(it, every[r * L:].data_ptr())
+            run.combine(it, every.data_ptr(), G)
+            run.finish_rounded(it)
+            gathered.append(every.view(G, L).cpu().numpy().copy())
+        got = run.result()
+        run.close()
+    return got, gathered
+
+
+def test_compact_exchange(ctx):
+    """SURVEY.md 8(e)'s exchange (dist.integrate(transport="compact")): every
+    rank's slice rounded on its own, the ranks' d*n_bins+2 doubles summed in
+    rank order.  One rank is bitwise the exact path; G ranks are
+    deterministic, stay within the rounding of the partial sums of it, count
+    the same samples, and every iteration's estimate and variance are the
+    gathered per-rank values added in rank order, bit for bit."""
+    d = 5
+    cfg = M.RunConfig(dims=d, maxcalls=2 * 10 ** 6, itmax=5, ita=3, tau_rel=1e-15, seed=3, lower=[0.0] * d,
+                      upper=[1.0] * d)
+    f = M.make_suite_integrand(2, d)
+    want = M.integrate(f, cfg, ctx=ctx)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    try:
+        one, _ = _compact_run(f, cfg, ctx, 1, stream)
+        assert [bits(h.estimate) for h in one.history] == [bits(h.estimate) for h in want.history]
+        assert [bits(h.variance) for h in one.history] == [bits(h.variance) for h in want.history]
+        assert bits(one.estimate) == bits(want.estimate) and one.total_samples == want.total_samples
+        for G in (2, 3, 8):
+            got, gathered = _compact_run(f, cfg, ctx, G, stream)
+            again, _ = _compact_run(f, cfg, ctx, G, stream)
+            assert [bits(h.estimate) for h in got.history] == [bits(h.estimate) for h in again.history], G
+            assert got.iterations_used == want.iterations_used and got.total_samples == want.total_samples
+            for it, (a, b) in enumerate(zip(got.history, want.history)):
+                assert abs(a.estimate - b.estimate) <= 1e-13 * abs(b.estimate), (G, a, b)
+                assert abs(a.variance - b.variance) <= 1e-12 * b.variance, (G, a, b)
+                g = gathered[it]
+                est, var = float(g[0, 0]), float(g[0, 1])
+                for r in range(1, G):
+                    est, var = est + float(g[r, 0]), var + float(g[r, 1])
+                assert bits(a.estimate) == bits(est) and bits(a.variance) == bits(var), (G, it)
+                # samples counted on the device, summed over the ranks
+                assert int(g[:, 2].view(np.uint64).sum()) == want.total_samples // cfg.itmax, (G, it)
+    finally:
+        ctx.set_stream(0)
+
+
 def test_convergence_behaviour_matches_reference_8d(golden, ctx):
     """BASELINE config 2 style: the time-to-epsrel run converges at the same
     iteration as the reference (same tau, chi2 gate, schedule)."""
