@@ -198,6 +198,25 @@ inline Shape make_shape(std::uint32_t dims, std::uint32_t nb, std::uint64_t m, s
   return sh;
 }
 
+/// Device buffers of one Run (mcubes.cuh): its grid, bounds, contributions,
+/// history, state, error key and exchange words -- exclusively its own while
+/// it lives, recycled through the Context's pool afterwards (cudaMalloc and
+/// the device-synchronising cudaFree cost ~50 us per integrate() call
+/// otherwise).
+struct RunBufs {
+  DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var;
+  DevBuf<unsigned long long> words, err_key;
+  DevBuf<RunState> state;
+  cudaEvent_t released = nullptr;  ///< recorded on the releasing run's stream
+  bool pending = false;            ///< `released` marks work a reuser must wait for
+  RunBufs() = default;
+  RunBufs(const RunBufs&) = delete;
+  RunBufs& operator=(const RunBufs&) = delete;
+  ~RunBufs() {
+    if (released) cudaEventDestroy(released);
+  }
+};
+
 /// A device context: one CUDA device, one stream, reusable scratch.
 /// Use from one host thread at a time; separate contexts may run concurrently.
 class Context {
@@ -270,6 +289,28 @@ class Context {
   /// (0 = not run, 1 = continue, 2 = stop), for integrate()'s bounded lookahead.
   static constexpr std::uint32_t kMaxFlagIterations = 16384;
   int* host_flags() const { return flags_; }
+  /// A Run's buffer set: a recycled one when available (stream-ordered after
+  /// the work of the run that released it), else a new one.
+  std::unique_ptr<RunBufs> acquire_run_bufs() {
+    if (run_pool_.empty()) return std::make_unique<RunBufs>();
+    std::unique_ptr<RunBufs> b = std::move(run_pool_.back());
+    run_pool_.pop_back();
+    if (b->pending) {  // the releasing run's kernels may still be in flight on another stream
+      MCB_CUDA(cudaStreamWaitEvent(stream_, b->released, 0));
+      b->pending = false;
+    }
+    return b;
+  }
+  /// Return a Run's buffers after its last enqueued work (stream order).
+  void release_run_bufs(std::unique_ptr<RunBufs> b) noexcept {
+    if (!b) return;
+    if (!b->released && cudaEventCreateWithFlags(&b->released, cudaEventDisableTiming) != cudaSuccess) return;
+    if (cudaEventRecord(b->released, stream_) != cudaSuccess) return;  // dropped: freed instead of pooled
+    b->pending = true;
+    if (run_pool_.size() < kRunPool) run_pool_.push_back(std::move(b));
+  }
+  static constexpr std::size_t kRunPool = 8;
+
   /// The i-th event of a reusable pool (created on first use).
   cudaEvent_t event(std::size_t i) {
     while (events_.size() <= i) {
@@ -291,6 +332,7 @@ class Context {
   bool staging_live_ = false;
   int* flags_ = nullptr;
   std::vector<cudaEvent_t> events_;
+  std::vector<std::unique_ptr<RunBufs>> run_pool_;
 };
 
 /// Geometry of one K1 launch (results do not depend on it).

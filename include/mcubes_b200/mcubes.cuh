@@ -641,7 +641,8 @@ namespace gpu {
 /// between sample() and finish().  integrate() below is the single-GPU loop.
 class Run {
  public:
-  Run(Context& ctx, IntegrandOps ops, const RunConfig& cfg) : ctx_(ctx), ops_(std::move(ops)), cfg_(cfg) {
+  Run(Context& ctx, IntegrandOps ops, const RunConfig& cfg)
+      : ctx_(ctx), bufs_(ctx.acquire_run_bufs()), b_(*bufs_), ops_(std::move(ops)), cfg_(cfg) {
     sp_ = setup(cfg_);
     sh_ = make_shape(cfg_.dims, cfg_.n_bins, sp_.m, sp_.s, sp_.p);
     ctx_.activate();
@@ -679,6 +680,10 @@ class Run {
       zero_exchange();
     }
   }
+
+  ~Run() { ctx_.release_run_bufs(std::move(bufs_)); }
+  Run(const Run&) = delete;
+  Run& operator=(const Run&) = delete;
 
   /// Resume from a checkpoint: the grid in force after `history.size()`
   /// completed iterations and their results.  The stream is keyed by
@@ -983,12 +988,10 @@ class Run {
   Context& ctx_;
   /// The run's own device buffers: nothing else enqueued on the context
   /// (a standalone v_sample, Grid::adjusted, another Run, e.g. from an
-  /// observer) can replace this run's grid, state or exchange words.
-  struct Bufs {
-    DevBuf<double> edges, lower, upper, contrib, hist_est, hist_var;
-    DevBuf<unsigned long long> words, err_key;
-    DevBuf<RunState> state;
-  } b_;
+  /// observer) can replace this run's grid, state or exchange words.  They
+  /// come from the context's pool and go back to it when the run ends.
+  std::unique_ptr<RunBufs> bufs_;
+  RunBufs& b_;
   IntegrandOps ops_;
   RunConfig cfg_;
   SetupParams sp_{};
