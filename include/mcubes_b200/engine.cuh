@@ -51,11 +51,11 @@ inline bool pdl_enabled() {
   return on;
 }
 
-/// MCB_K1_CLUSTER=0: K1 without 2-CTA clusters (each CTA flushes its own words).
-inline bool k1_cluster_enabled() {
+/// MCB_K1_CLUSTER=1: K1 in 2-CTA clusters (each CTA flushes half of both CTAs' words over DSMEM).
+inline bool k1_cluster_enabled() {  // off by default since round 2 (DESIGN.md section 4 table)
   static const bool on = [] {
     const char* v = std::getenv("MCB_K1_CLUSTER");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }

@@ -272,6 +272,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     bad[tid] = 0;
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(0);
   const std::uint32_t total_el = D * n;
   for (std::uint32_t idx = tid; idx < total_el; idx += nthreads) {  // smoothing (grid.hpp:240-252)
     const std::uint32_t j = idx / n, i = idx - j * n;
@@ -285,6 +286,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     smooth_of(j)[i] = v;
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(1);
   if (n == 1) return;  // a single bin has no interior edge
   if (tid < static_cast<int>(D) && any[tid]) {  // the smoothed total, in order
     const double* sm = smooth_of(tid);
@@ -294,6 +296,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     tot[tid] = t;
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(2);
   for (std::uint32_t idx = tid; idx < total_el; idx += nthreads) {  // importance (grid.hpp:255-262)
     const std::uint32_t j = idx / n, i = idx - j * n;
     if (!any[j]) continue;
@@ -305,6 +308,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     sm[n + i] = r;
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(3);
   if (tid < static_cast<int>(D) && any[tid]) {  // cumulative importance and targets, in order
     double* sm = smooth_of(tid);
     const double* imp = sm + n;
@@ -336,6 +340,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     }
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(4);
   const std::uint32_t walk_el = D * (n - 1);
   for (std::uint32_t idx = tid; idx < walk_el; idx += nthreads) {  // the equal-share walk (grid.hpp:263-284)
     const std::uint32_t j = idx / (n - 1), i = idx - j * (n - 1);
@@ -358,6 +363,7 @@ __device__ inline void adjust_grid_par(const AdjustArgs& a, const double* contri
     sm[4 * n + i] = left + width * ((t - P[k]) / imp[k]);  // out row (after T)
   }
   bar_sync_n(1, nthreads);
+  MCB_ADJ_STAMP(5);
   for (std::uint32_t idx = tid; idx < walk_el; idx += nthreads) {  // strictly increasing?
     const std::uint32_t j = idx / (n - 1), i = idx - j * (n - 1);
     if (!any[j]) continue;

@@ -664,16 +664,18 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
     const std::uint32_t* peer_bins = peer_acc + kScalarAccs * kLaneCopies * kXWords;
     const int ncells = static_cast<int>(a.bin_n * nb);
     const int nbw = ncells * kXWords;
-    const int b0 = csize == 2 ? (crank ? nbw / 2 : 0) : 0, b1 = csize == 2 ? (crank ? nbw : nbw / 2) : nbw;
-    for (int i = b0 + tid; i < b1; i += nt) {
-      const unsigned long long v = static_cast<unsigned long long>(bins[i]) +
-                                   (csize == 2 ? static_cast<unsigned long long>(peer_bins[i]) : 0ull);
-      if (!v) continue;
+    auto flush_bin_word = [&](int i, unsigned long long v) {  // block word i (cell-major) -> exchange slot
       const int c = i / kXWords, w = i - c * kXWords;
       const int ax = c / static_cast<int>(nb), cell = c - ax * static_cast<int>(nb);
       const int slot = (static_cast<int>(a.bin_lo) + ax) * static_cast<int>(a.nb_out) +
                        min(cell, static_cast<int>(a.nb_out) - 1);
       add_word(static_cast<std::ptrdiff_t>(kScalarAccs + slot) * kXWords + w, v);
+    };
+    const int b0 = csize == 2 ? (crank ? nbw / 2 : 0) : 0, b1 = csize == 2 ? (crank ? nbw : nbw / 2) : nbw;
+    for (int i = b0 + tid; i < b1; i += nt) {
+      const unsigned long long v = static_cast<unsigned long long>(bins[i]) +
+                                   (csize == 2 ? static_cast<unsigned long long>(peer_bins[i]) : 0ull);
+      if (v) flush_bin_word(i, v);
     }
     // est+/est-/var: the 32 lane copies (of both CTAs) folded into u64 word sums (< 2^38, exact)
     const int nsw = scalars ? kScalarAccs * kXWords : 0;  // later passes deposit bins only

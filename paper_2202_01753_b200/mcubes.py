@@ -613,10 +613,13 @@ class RunConfig:
     bins: str = ""
 
     def _c(self):
-        lo, hi = _f64(self.lower), _f64(self.upper)
+        # plain ctypes arrays (a numpy round trip costs ~10 us per integrate() call)
+        lo = (C.c_double * len(self.lower))(*self.lower)
+        hi = (C.c_double * len(self.upper))(*self.upper)
         c = L.mcb_config(self.dims, self.n_bins, self.maxcalls, self.itmax, self.ita, self.tau_rel, self.alpha,
                          self.chi2_dof_max, self.seed, int(self.variant), self.workers,
-                         _dptr(lo) if lo.size else None, _dptr(hi) if hi.size else None,
+                         C.cast(lo, C.POINTER(C.c_double)) if len(self.lower) else None,
+                         C.cast(hi, C.POINTER(C.c_double)) if len(self.upper) else None,
                          rng_code(self.rng, self.bins), 0)
         return c, (lo, hi)
 

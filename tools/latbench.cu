@@ -137,7 +137,7 @@ int main(int argc, char** argv) {
       std::printf("finish phases (us from start): blocks done %.2f  last block in %.2f  staged %.2f  adjusted %.2f  end %.2f\n",
                   (tt[1] - tt[0]) * 1e-3, (tt[2] - tt[0]) * 1e-3, (tt[3] - tt[0]) * 1e-3, (tt[4] - tt[0]) * 1e-3,
                   (tt[5] - tt[0]) * 1e-3);
-      std::printf("adjust axis 0 (us from start): loaded %.2f total %.2f imp %.2f sums %.2f walk %.2f check %.2f stored %.2f\n",
+      std::printf("adjust (us from start): staged %.2f smoothed %.2f total %.2f importance %.2f sums %.2f walk %.2f [6] %.2f\n",
                   (tt[8] - tt[0]) * 1e-3, (tt[9] - tt[0]) * 1e-3, (tt[10] - tt[0]) * 1e-3, (tt[11] - tt[0]) * 1e-3,
                   (tt[12] - tt[0]) * 1e-3, (tt[13] - tt[0]) * 1e-3, (tt[14] - tt[0]) * 1e-3);
     }
