@@ -422,7 +422,11 @@ Launch launch_k1(Context& ctx, const F& f, const Shape& sh, std::uint32_t bin_ax
   }
   const int occ = std::max(cached_occ, 1);
   const std::uint64_t work = n1 > n0 ? n1 - n0 : 0;
-  const std::uint64_t want = (work + kThreads - 1) / kThreads;
+  // Blocks: every SM once the work fills a warp per SM.  Small problems
+  // (fewer work items than one full block per SM, e.g. 10D at 1e6 calls:
+  // 59,049 cubes of 16 samples) then spread over all SMs with fewer threads
+  // each instead of filling a few SMs with full blocks.
+  const std::uint64_t want = (work + 31) / 32;
   L.blocks = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, std::uint64_t(ctx.sms()) * occ)));
   // Threads per block: the fewest (whole warps) that keep the per-thread cube
   // count of a full block.  Small problems then run every thread over the

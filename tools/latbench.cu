@@ -168,8 +168,13 @@ int main(int argc, char** argv) {
       ++n;
     }
   }
-  std::printf("rng=%d D=%d maxcalls=%llu m=%llu p=%llu  per iteration (us): sample %.1f  reduce %.1f  finish %.1f\n",
+  const IntegrationResult res = run.result();
+  std::uint64_t eb;
+  std::memcpy(&eb, &res.estimate, 8);
+  std::printf("rng=%d D=%d maxcalls=%llu m=%llu p=%llu  per iteration (us): sample %.1f  reduce %.1f  finish %.1f"
+              "  estimate bits %016llx\n",
               rngk, D, (unsigned long long)maxcalls, (unsigned long long)run.params().m,
-              (unsigned long long)run.params().p, 1e3 * t[0] / n, 1e3 * t[1] / n, 1e3 * t[2] / n);
+              (unsigned long long)run.params().p, 1e3 * t[0] / n, 1e3 * t[1] / n, 1e3 * t[2] / n,
+              (unsigned long long)eb);
   return 0;
 }
