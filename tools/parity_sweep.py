@@ -30,7 +30,8 @@ def main():
     rng = np.random.default_rng(2026)
     stats = {}
     for t in range(trials):
-        stream = ("compat", "philox")[t % 2]
+        stream = ("compat", "philox", "philox_exact")[t % 3]
+        mrng, mbins = ("philox", "exact") if stream == "philox_exact" else (stream, "")
         d = int(rng.integers(1, 11))
         g = int(rng.integers(1, max(2, int(200000 ** (1 / d))) + 1))
         m = g ** d
@@ -45,15 +46,17 @@ def main():
         f = M.IntegrandSpec("f", d, lo, hi, fam)
         grid = M.Grid(d, nb, lo, hi)
         if mode == "frozen":
-            r = M.v_sample_no_adjust(f, grid, m, 1, p, seed, it, ctx=ctx, rng=stream)
+            r = M.v_sample_no_adjust(f, grid, m, 1, p, seed, it, ctx=ctx, rng=mrng)
             est, var, contrib = r.raw_estimate, r.raw_variance, None
         else:
             r = M.v_sample(f, grid, m, 1, p, seed, it,
-                           M.BinUpdate.axis0_only if mode == "axis0" else M.BinUpdate.all_axes, ctx=ctx, rng=stream)
+                           M.BinUpdate.axis0_only if mode == "axis0" else M.BinUpdate.all_axes, ctx=ctx, rng=mrng,
+                           bins=mbins)
             est, var, contrib = r.raw_estimate, r.raw_variance, r.contributions.values
         same = bits(est) == bits(want["est"]) and bits(var) == bits(want["var"])
         if contrib is not None:
             same = same and np.array_equal(np.asarray(contrib).view(np.uint64), np.asarray(want["contrib"]).view(np.uint64))
+            assert r.contributions.writes() == want["writes"], (stream, d, m, p, nb, mode)  # device-counted deposits
         rel = abs(est - want["est"]) / max(abs(want["est"]), 1e-300)
         key = (stream, "f%d" % fam)
         s = stats.setdefault(key, [0, 0, 0.0])
@@ -63,7 +66,8 @@ def main():
         if fam == 2 and not same:
             print("MISMATCH", stream, d, m, p, nb, seed, it, mode, flush=True)
     print("# tools/parity_sweep.py %d trials: B200 v_sample / v_sample_no_adjust vs the C oracle" % trials)
-    print("# (compat: the reference's arithmetic; philox: its C twin).  f2 is +-*/ only: must be bitwise.")
+    print("# (compat: the reference's arithmetic; philox / philox_exact: its C twin, 24-bit / exact bins).")
+    print("# f2 is +-*/ only: must be bitwise.  Device-counted writes equal the oracle's in every adjusting case.")
     print("%-8s %-4s %7s %9s %14s" % ("stream", "f", "trials", "bitwise", "max rel diff"))
     for (stream, fam), (n, same, rel) in sorted(stats.items()):
         print("%-8s %-4s %7d %9d %14.3e" % (stream, fam, n, same, rel))
