@@ -439,6 +439,11 @@ def run_ours(args, rank, world, local_rank):
         tte = time_to_epsrel_dist(M, ctx, dist, dev, rank, args.transport)
         if rank == 0:
             line["time_to_epsrel"] = tte
+    if not args.no_cpu:
+        tte = time_to_epsrel_headline(M, ctx, dist if world > 1 else None, dev, rank, world, args,
+                                      with_cpu=rank == 0 and world == 1)
+        if rank == 0:
+            line["time_to_epsrel_headline"] = tte
     if rank == 0:
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
@@ -545,6 +550,53 @@ def time_to_epsrel(M, ctx, runs: int = 2, cpu_budget_s: float = 120.0):
     return {"protocol": f"8D f1..f6, maxcalls 1e7, itmax 30, ita 10; tau 1e-3 / 5^k, {runs} seeds per level, "
                         "a stream stops tightening once < 50% converge (mcubes_bench.cpp:145-165)",
             "cpu_threads": threads, "cpu_seconds": cpu_used, "levels": rows}
+
+
+def time_to_epsrel_headline(M, ctx, dist, dev, rank, world, args, with_cpu):
+    """time_to_epsrel at the headline size, where GPUs matter: 8D f4 at the
+    bench's maxcalls (1e9: 8.6e8 evals per iteration) to tau_rel 3e-5, on
+    this launch's GPUs (dist.integrate over the ranks for N > 1, wall time
+    max over ranks), both streams; at N = 1 also the reference CPU integrate
+    on the host cores (same schedule and seed; its stream is compat's)."""
+    import torch
+
+    import oracle as O
+    from paper_2202_01753_b200 import dist as mdist
+
+    d, tau, itmax, ita, seed = DIMS, 3e-5, 8, 6, 1  # bounded: <= 8 reference iterations of ~4.6 s
+    out = {"protocol": f"8D f4, maxcalls {args.maxcalls:.0e}, tau_rel {tau:g}, itmax {itmax}, ita {ita}, seed {seed}",
+           "gpus": world}
+    f = M.make_suite_integrand(FAMILY, d)
+    for rng, bins in (("philox", "r24"), ("compat", "")):
+        cfg = M.RunConfig(dims=d, maxcalls=args.maxcalls, itmax=itmax, ita=ita, tau_rel=tau, seed=seed,
+                          lower=[0.0] * d, upper=[1.0] * d, rng=rng, bins=bins)
+        run = (lambda: mdist.integrate(f, cfg, ctx=ctx, transport=args.transport)) if dist is not None else \
+            (lambda: M.integrate(f, cfg, ctx=ctx))
+        run()  # warm
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = run()
+        ms = 1e3 * (time.perf_counter() - t0)
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        out[f"gpu_{rng}"] = {"ms": ms, "iterations": r.iterations_used, "converged": r.converged,
+                             "estimate": r.estimate, "sigma": r.sigma, "chi2_dof": r.chi2_dof}
+    if with_cpu and O.ref_available():
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        o = O.integrate("ref", FAMILY, None, d, N_BINS, args.maxcalls, itmax, ita, tau, ALPHA, 1.5, seed, 0,
+                        [0.0] * d, [1.0] * d, workers=threads)
+        cms = 1e3 * (time.perf_counter() - t0)
+        out["cpu_reference"] = {"ms": cms, "iterations": o["iterations_used"], "converged": o["converged"],
+                                "estimate": o["estimate"], "sigma": o["sigma"], "threads": threads}
+        out["speedup_compat"] = cms / out["gpu_compat"]["ms"]
+        out["speedup_philox"] = cms / out["gpu_philox"]["ms"]
+        out["compat_same_iterations"] = o["iterations_used"] == out["gpu_compat"]["iterations"]
+    return out
 
 
 def time_to_epsrel_dist(M, ctx, dist, dev, rank, transport="collective"):
