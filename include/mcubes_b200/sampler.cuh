@@ -220,24 +220,15 @@ __device__ __forceinline__ double sample_point_fast(const SampleArgs& a, const F
     // (digit < 2^21), so z is one I2F.U64 and one DMUL: z = RN((digit 2^32 + r) cs).
     double z;
     if constexpr (sizeof(Dig) == 4) {
-#if MCB_K1_ZASM
-      // the same bits without the I2F: 2^52 + digit:r is the double with words
-      // {0x43300000 | digit, r} (digit < 2^20); subtracting 2^52 is exact
+      // 2^52 + digit:r is the double with words {0x43300000 | digit, r}
+      // (digit < 2^20); subtracting 2^52 is exact (no I2F on the XU pipe)
       z = __dmul_rn(__dadd_rn(__hiloint2double(static_cast<int>(0x43300000u | dig[j]), static_cast<int>(r[j])),
                               -0x1p52),
                     a.cs);
-#else
-      z = __dmul_rn(__ull2double_rn((static_cast<std::uint64_t>(dig[j]) << 32) | r[j]), a.cs);
-#endif
     } else {
       z = __fma_rn(__uint2double_rn(r[j]), a.cs, __dmul_rn(__ull2double_rn(dig[j]), a.nbg));
     }
-#if MCB_K1_FLOOR
-    // floor(z) on the FP64 pipe: 2^52 + z rounded down has ulp 1, its low word is floor(z)
-    const std::uint32_t i = static_cast<std::uint32_t>(__double2loint(__dadd_rd(z, 0x1p52)));
-#else
     const std::uint32_t i = __double2uint_rz(z);  // 0 <= z <= nb: no clamp (padded table)
-#endif
     const double2 lw = lds_d2(lw_s + (static_cast<std::uint32_t>(j) * pnb + i) * C * 16u);  // lane's copy
     x[j] = __fma_rn(z, lw.y, lw.x);
     jw = j == 0 ? lw.y : __dmul_rn(jw, lw.y);
@@ -581,24 +572,12 @@ __global__ void __launch_bounds__(sample_threads(R, D), 1) vsample_kernel(const 
         sum = __dadd_rn(sum, fj);
         // Welford with y = RN(1/n): mean += (f - mean) * y
         const std::uint32_t nk = k + 1;
-#if MCB_K1_RCPSEL
         double y;
         if (nk <= 2) y = nk == 1 ? 1.0 : 0.5;  // p = 2 (every BASELINE shape above 1e6 calls): no LDS
         else y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
-#else
-        const double y = nk < static_cast<std::uint32_t>(kRcpSmem) ? rcp[nk] : __drcp_rn(static_cast<double>(nk));
-#endif
-#if MCB_K1_PEEL
-        if (k == 0) {  // y = 1: the general update gives mean = fj, m2 = 0 (a zero's sign never reaches m2)
-          mean = fj;
-          m2 = 0.0;
-        } else
-#endif
-        {
-          const double dd = __dsub_rn(fj, mean);
-          mean = __fma_rn(dd, y, mean);
-          m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
-        }
+        const double dd = __dsub_rn(fj, mean);
+        mean = __fma_rn(dd, y, mean);
+        m2 = __fma_rn(dd, __dsub_rn(fj, mean), m2);
         if (bin_n) deposit(fj, bin);
       }
       sum = __dmul_rn(sum, a.scale);
