@@ -5,7 +5,7 @@
 // prints evals/s plus the run's final estimate bits (identical across
 // variants: the sums are exact).
 //   nvcc ... -DMCB_SAMPLE_THREADS_PHILOX=768 tools/k1bench.cu
-//   ./k1bench [maxcalls] [reps] [rng: 0 compat, 1 philox] [frozen: 0|1] [warm iterations]
+//   ./k1bench [maxcalls] [reps] [rng: 0 compat, 1 philox, 2 philox with exact bins] [frozen: 0|1] [warm iterations]
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -33,8 +33,9 @@ int main(int argc, char** argv) {
   cfg.tau_rel = 1e-15;
   gpu::Context ctx(0);
   const gpu::fn::F4 f{};
-  const gpu::IntegrandOps ops = rngk ? gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox>(f)
-                                     : gpu::make_ops<gpu::fn::F4, gpu::RngKind::compat>(f);
+  const gpu::IntegrandOps ops = rngk == 2 ? gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox_exact>(f)
+                                : rngk ? gpu::make_ops<gpu::fn::F4, gpu::RngKind::philox>(f)
+                                       : gpu::make_ops<gpu::fn::F4, gpu::RngKind::compat>(f);
   if (direct_key >= 0) {  // uniform grid, fixed iteration key, no Run
     const SetupParams sp = setup(cfg);
     const gpu::Shape sh = gpu::make_shape(D, 50, sp.m, 1, sp.p);
