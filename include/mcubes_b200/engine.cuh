@@ -301,6 +301,9 @@ class Context {
     }
     return b;
   }
+  /// Liveness token: a Run that outlives its context frees its buffers
+  /// instead of returning them to the (destroyed) pool.
+  std::weak_ptr<const int> alive() const { return alive_; }
   /// Return a Run's buffers after its last enqueued work (stream order).
   void release_run_bufs(std::unique_ptr<RunBufs> b) noexcept {
     if (!b) return;
@@ -333,6 +336,7 @@ class Context {
   int* flags_ = nullptr;
   std::vector<cudaEvent_t> events_;
   std::vector<std::unique_ptr<RunBufs>> run_pool_;
+  std::shared_ptr<const int> alive_ = std::make_shared<const int>(1);
 };
 
 /// Geometry of one K1 launch (results do not depend on it).

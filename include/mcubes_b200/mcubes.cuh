@@ -681,7 +681,9 @@ class Run {
     }
   }
 
-  ~Run() { ctx_.release_run_bufs(std::move(bufs_)); }
+  ~Run() {
+    if (!ctx_alive_.expired()) ctx_.release_run_bufs(std::move(bufs_));  // else bufs_ just frees its memory
+  }
   Run(const Run&) = delete;
   Run& operator=(const Run&) = delete;
 
@@ -992,6 +994,7 @@ class Run {
   /// come from the context's pool and go back to it when the run ends.
   std::unique_ptr<RunBufs> bufs_;
   RunBufs& b_;
+  std::weak_ptr<const int> ctx_alive_ = ctx_.alive();
   IntegrandOps ops_;
   RunConfig cfg_;
   SetupParams sp_{};

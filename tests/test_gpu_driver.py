@@ -235,6 +235,41 @@ def test_compact_exchange(ctx):
         ctx.set_stream(0)
 
 
+def test_run_buffers_pool_and_lifetimes():
+    """Runs take their device buffers from the context's pool: back-to-back
+    runs of different shapes reuse and grow them with identical results, a
+    run stepped while another run of the same context lives keeps its own
+    state, and a run destroyed after its context frees its buffers."""
+    d = 4
+    cfg_a = M.RunConfig(dims=d, maxcalls=10 ** 5, itmax=4, ita=2, tau_rel=1e-15, seed=5, lower=[0.0] * d,
+                        upper=[1.0] * d)
+    cfg_b = M.RunConfig(dims=6, maxcalls=10 ** 6, itmax=3, ita=3, tau_rel=1e-15, seed=9, lower=[0.0] * 6,
+                        upper=[1.0] * 6)
+    fa, fb = M.make_suite_integrand(2, d), M.make_suite_integrand(4, 6)
+    c = M.Context(0)
+    want_a, want_b = M.integrate(fa, cfg_a, ctx=c), M.integrate(fb, cfg_b, ctx=c)
+    for _ in range(3):  # pooled buffers, alternating sizes
+        assert bits(M.integrate(fa, cfg_a, ctx=c).estimate) == bits(want_a.estimate)
+        assert bits(M.integrate(fb, cfg_b, ctx=c).estimate) == bits(want_b.estimate)
+    ra, rb = M.Run(fa, cfg_a, c), M.Run(fb, cfg_b, c)  # two live runs, interleaved
+    for it in range(1, 4):
+        ra.step(it)
+        rb.step(it)
+    ra.step(4)
+    assert bits(ra.result().estimate) == bits(want_a.estimate)
+    assert bits(rb.result().estimate) == bits(want_b.estimate)
+    rb.close()
+    c2 = M.Context(0)
+    r2 = M.Run(fa, cfg_a, c2)
+    for it in range(1, 5):
+        r2.step(it)
+    assert bits(r2.result().estimate) == bits(want_a.estimate)
+    c2.close()  # the context goes first
+    r2.close()  # the run frees its buffers instead of pooling them
+    ra.close()
+    c.close()
+
+
 def test_convergence_behaviour_matches_reference_8d(golden, ctx):
     """BASELINE config 2 style: the time-to-epsrel run converges at the same
     iteration as the reference (same tau, chi2 gate, schedule)."""
