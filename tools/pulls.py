@@ -1,6 +1,10 @@
 """Per-iteration pull distribution (estimate - truth) / sigma_iteration over
-seeds, compat vs philox, for a peaked integrand (8D f2 at 1e7 calls): checks
-the Philox path for bias beyond the reference's own early-iteration bias."""
+seeds, per stream (compat = the reference bit for bit, philox = 24-bit bins,
+philox_exact): checks the Philox paths for bias beyond the reference's own
+early-iteration bias.
+
+    python tools/pulls.py FAMILY DIMS MAXCALLS SEEDS [compat,philox,philox_exact]
+"""
 import math
 import os
 import sys
@@ -18,13 +22,16 @@ its = 8
 ctx = M.Context(0)
 f = M.make_suite_integrand(fam, d)
 truth = f.reference
-for rng in ("compat", "philox"):
+streams = sys.argv[5].split(",") if len(sys.argv) > 5 else ["compat", "philox"]
+for stream in streams:
+    rng, bins = ("philox", "exact") if stream == "philox_exact" else (stream, "")
     P = np.zeros((nseed, its))
     for s in range(nseed):
         cfg = M.RunConfig(dims=d, maxcalls=mc, itmax=its, ita=its, tau_rel=1e-15, seed=s, lower=[0.0] * d,
-                          upper=[1.0] * d, rng=rng)
+                          upper=[1.0] * d, rng=rng, bins=bins)
         r = M.integrate(f, cfg, ctx=ctx)
         for i, h in enumerate(r.history):
             P[s, i] = (h.estimate - truth) / math.sqrt(h.variance)
-    print(f"f{fam} {d}D {mc:.0e} {rng:7s} mean pull per iteration: " + " ".join(f"{x:6.2f}" for x in P.mean(0)))
-    print(f"f{fam} {d}D {mc:.0e} {rng:7s}  std pull per iteration: " + " ".join(f"{x:6.2f}" for x in P.std(0)))
+    print(f"f{fam} {d}D {mc:.0e} {stream:12s} mean pull per iteration: " + " ".join(f"{x:6.2f}" for x in P.mean(0))
+          + f"   ({nseed} seeds)")
+    print(f"f{fam} {d}D {mc:.0e} {stream:12s}  std pull per iteration: " + " ".join(f"{x:6.2f}" for x in P.std(0)))
