@@ -221,20 +221,24 @@ inline void download(Context& ctx, double* host, const double* dev, std::size_t 
 /// row-major, implicit left edge at `lower`.
 class Grid {
  public:
+  /// The uniform grid (grid.hpp:30-50): n_bins equal bins per axis, edge i
+  /// at lower + (i + 1) * width, the last edge exactly the upper bound.
   Grid(std::uint32_t dims, std::uint32_t n_bins, std::span<const double> lower, std::span<const double> upper)
-      : dims_(dims), n_bins_(n_bins), lower_(lower.begin(), lower.end()), upper_(upper.begin(), upper.end()),
-        edges_(std::size_t{dims} * n_bins) {
-    if (dims_ == 0) throw std::invalid_argument("Grid: dims must be >= 1");
-    if (n_bins_ < 2) throw std::invalid_argument("Grid: n_bins must be >= 2");
-    if (lower_.size() != dims_ || upper_.size() != dims_)
-      throw std::invalid_argument("Grid: bounds must have one entry per axis");
+      : dims_(dims), n_bins_(n_bins), lower_(lower.begin(), lower.end()), upper_(upper.begin(), upper.end()) {
+    const auto need = [](bool ok, const char* what) {
+      if (!ok) throw std::invalid_argument(std::string("Grid: ") + what);
+    };
+    need(dims_ != 0, "dims must be >= 1");
+    need(n_bins_ >= 2, "n_bins must be >= 2");
+    need(lower_.size() == dims_ && upper_.size() == dims_, "bounds must have one entry per axis");
+    for (std::uint32_t j = 0; j < dims_; ++j)
+      need(lower_[j] < upper_[j] && std::isfinite(lower_[j]) && std::isfinite(upper_[j]),
+           "requires finite lower < upper on every axis");
+    edges_.reserve(std::size_t{dims_} * n_bins_);
     for (std::uint32_t j = 0; j < dims_; ++j) {
-      if (!(lower_[j] < upper_[j]) || !std::isfinite(lower_[j]) || !std::isfinite(upper_[j]))
-        throw std::invalid_argument("Grid: requires finite lower < upper on every axis");
-      double* row = edges_.data() + std::size_t{j} * n_bins_;
-      const double width = (upper_[j] - lower_[j]) / static_cast<double>(n_bins_);
-      for (std::uint32_t i = 0; i + 1 < n_bins_; ++i) row[i] = lower_[j] + static_cast<double>(i + 1) * width;
-      row[n_bins_ - 1] = upper_[j];
+      const double step = (upper_[j] - lower_[j]) / static_cast<double>(n_bins_);
+      for (std::uint32_t k = 1; k < n_bins_; ++k) edges_.push_back(lower_[j] + static_cast<double>(k) * step);
+      edges_.push_back(upper_[j]);
     }
   }
 
@@ -258,14 +262,9 @@ class Grid {
   [[nodiscard]] const std::vector<double>& lowers() const { return lower_; }
   [[nodiscard]] const std::vector<double>& uppers() const { return upper_; }
 
-  /// grid.hpp:61-67
-  [[nodiscard]] std::uint32_t bin_index(double u) const {
-    const double nb = static_cast<double>(n_bins_);
-    const double z = u * nb;
-    if (!(z > 0.0)) return 0;
-    if (z >= nb) return n_bins_ - 1;
-    return static_cast<std::uint32_t>(z);
-  }
+  /// grid.hpp:61-67: the bin of unit coordinate u, clamped to [0, n_bins - 1]
+  /// (u <= 0 or NaN -> 0).
+  [[nodiscard]] std::uint32_t bin_index(double u) const { return clamp_bin(u * static_cast<double>(n_bins_)); }
   void bin_indices(std::span<const double> u, std::span<std::uint32_t> out) const {
     for (std::uint32_t j = 0; j < dims_; ++j) out[j] = bin_index(u[j]);
   }
@@ -296,28 +295,38 @@ class Grid {
     return adjust_on_device(c, alpha, true);
   }
 
-  /// Plain-text form (grid.hpp:148-158).
+  /// Plain-text checkpoint (grid.hpp:148-158): a "dims n_bins" header, then
+  /// one line per axis -- lower, upper and the n_bins right edges -- at 17
+  /// significant digits, which round-trip every double.
   void write(std::ostream& os) const {
+    const std::streamsize saved = os.precision(17);
     os << dims_ << ' ' << n_bins_ << '\n';
-    const auto saved = os.precision(17);
     for (std::uint32_t j = 0; j < dims_; ++j) {
+      std::span<const double> row = edges(j);
       os << lower_[j] << ' ' << upper_[j];
-      for (const double e : edges(j)) os << ' ' << e;
+      for (std::size_t k = 0; k < row.size(); ++k) os << ' ' << row[k];
       os << '\n';
     }
     os.precision(saved);
   }
 
-  /// grid.hpp:161-174
+  /// grid.hpp:161-174: parses write()'s format; a truncated or non-numeric
+  /// header, bound pair or edge list raises invalid_argument, as the reference.
   static Grid read(std::istream& is) {
+    const auto fail = [](const char* what) { throw std::invalid_argument(std::string("Grid::read: ") + what); };
     std::uint32_t dims = 0, n_bins = 0;
-    if (!(is >> dims >> n_bins) || dims == 0 || n_bins < 2) throw std::invalid_argument("Grid::read: malformed header");
-    std::vector<double> lower(dims), upper(dims), edges(std::size_t{dims} * n_bins);
+    is >> dims >> n_bins;
+    if (!is || dims == 0 || n_bins < 2) fail("malformed header");
+    std::vector<double> lower(dims), upper(dims), edges;
+    edges.reserve(std::size_t{dims} * n_bins);
     for (std::uint32_t j = 0; j < dims; ++j) {
-      if (!(is >> lower[j] >> upper[j])) throw std::invalid_argument("Grid::read: malformed axis bounds");
-      double* row = edges.data() + std::size_t{j} * n_bins;
-      for (std::uint32_t i = 0; i < n_bins; ++i)
-        if (!(is >> row[i])) throw std::invalid_argument("Grid::read: malformed edge list");
+      is >> lower[j] >> upper[j];
+      if (!is) fail("malformed axis bounds");
+      for (std::uint32_t k = 0; k < n_bins; ++k) {
+        double e;
+        if (!(is >> e)) fail("malformed edge list");
+        edges.push_back(e);
+      }
     }
     return Grid(dims, n_bins, std::move(lower), std::move(upper), std::move(edges));
   }
@@ -328,14 +337,13 @@ class Grid {
   Grid(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> lower, std::vector<double> upper,
        std::vector<double> raw_edges)
       : dims_(dims), n_bins_(n_bins), lower_(std::move(lower)), upper_(std::move(upper)), edges_(std::move(raw_edges)) {
+    // grid.hpp:61-67 invariants of a checkpointed grid: per axis, lower < e_0 < ... < e_{n-1} = upper
     for (std::uint32_t j = 0; j < dims_; ++j) {
       if (!(lower_[j] < upper_[j])) throw std::invalid_argument("Grid: requires lower < upper on every axis");
-      double prev = lower_[j];
-      for (const double e : edges(j)) {
-        if (!(e > prev)) throw std::invalid_argument("Grid: edges must increase strictly");
-        prev = e;
-      }
-      if (edges(j).back() != upper_[j]) throw std::invalid_argument("Grid: last edge must equal the upper bound");
+      const std::span<const double> row = edges(j);
+      for (std::size_t k = 0; k < row.size(); ++k)
+        if (!(row[k] > (k ? row[k - 1] : lower_[j]))) throw std::invalid_argument("Grid: edges must increase strictly");
+      if (row[row.size() - 1] != upper_[j]) throw std::invalid_argument("Grid: last edge must equal the upper bound");
     }
   }
 
@@ -365,21 +373,29 @@ class Grid {
     return g;
   }
 
+  /// Bin of the bin coordinate z = u * n_bins: floor(z) inside, 0 for z <= 0
+  /// (or NaN), n_bins - 1 for z >= n_bins (grid.hpp:61-67, 209-213).
+  [[nodiscard]] std::uint32_t clamp_bin(double z) const {
+    if (z >= static_cast<double>(n_bins_)) return n_bins_ - 1;
+    return z > 0.0 ? static_cast<std::uint32_t>(z) : 0u;
+  }
+
+  /// The host form of the map K1 applies (grid.hpp:204-224), operation for
+  /// operation the same IEEE arithmetic: x = left + (z - bin) * width and the
+  /// jacobian as the running product of n_bins * width, axis by axis.
   template <bool kWantBins>
   double transform_impl(std::span<const double> u, std::span<double> x, std::span<std::uint32_t> bins) const {
-    double jac = 1.0;
     const double nb = static_cast<double>(n_bins_);
+    double jac = 1.0;
     for (std::uint32_t j = 0; j < dims_; ++j) {
       const double z = u[j] * nb;
-      std::uint32_t i = 0;
-      if (z >= nb) i = n_bins_ - 1;
-      else if (z > 0.0) i = static_cast<std::uint32_t>(z);
-      const double* row = edges_.data() + std::size_t{j} * n_bins_;
-      const double left = i == 0 ? lower_[j] : row[i - 1];
-      const double width = row[i] - left;
-      x[j] = left + (z - static_cast<double>(i)) * width;
+      const std::uint32_t b = clamp_bin(z);
+      const std::span<const double> row = edges(j);
+      const double left = b ? row[b - 1] : lower_[j];
+      const double width = row[b] - left;
+      x[j] = left + (z - static_cast<double>(b)) * width;
       jac *= nb * width;
-      if constexpr (kWantBins) bins[j] = i;
+      if constexpr (kWantBins) bins[j] = b;
     }
     return jac;
   }
@@ -514,21 +530,25 @@ struct RunConfig {
   unsigned workers = 0;  ///< accepted for source compatibility; the GPU path ignores it
   gpu::RngKind rng = gpu::RngKind::compat;
 
+  /// driver.hpp:52-70: the same checks, in the same order, with the same
+  /// messages (the first failing one is reported).
   void validate() const {
-    if (dims < 1) throw std::invalid_argument("RunConfig: dims must be >= 1");
-    if (n_bins < 2) throw std::invalid_argument("RunConfig: n_bins must be >= 2");
-    if (dims >= 63 || maxcalls < (std::uint64_t{2} << dims))
-      throw std::invalid_argument("RunConfig: maxcalls must be >= 2*2^dims");
-    if (!(tau_rel > 0.0) || !(tau_rel < 1.0)) throw std::invalid_argument("RunConfig: tau_rel must lie in (0, 1)");
-    if (itmax < 1) throw std::invalid_argument("RunConfig: itmax must be >= 1");
-    if (ita > itmax) throw std::invalid_argument("RunConfig: ita must not exceed itmax");
-    if (!(alpha >= 0.0) || !std::isfinite(alpha)) throw std::invalid_argument("RunConfig: alpha must be finite and >= 0");
-    if (!(chi2_dof_max > 0.0)) throw std::invalid_argument("RunConfig: chi2_dof_max must be positive");
-    if (lower.size() != dims || upper.size() != dims)
-      throw std::invalid_argument("RunConfig: bounds must have one entry per axis");
-    for (std::uint32_t j = 0; j < dims; ++j)
-      if (!std::isfinite(lower[j]) || !std::isfinite(upper[j]) || !(lower[j] < upper[j]))
-        throw std::invalid_argument("RunConfig: requires finite lower < upper on every axis");
+    const auto need = [](bool ok, const char* what) {
+      if (!ok) throw std::invalid_argument(std::string("RunConfig: ") + what);
+    };
+    need(dims >= 1, "dims must be >= 1");
+    need(n_bins >= 2, "n_bins must be >= 2");
+    need(dims < 63 && maxcalls >= (std::uint64_t{2} << dims), "maxcalls must be >= 2*2^dims");
+    need(tau_rel > 0.0 && tau_rel < 1.0, "tau_rel must lie in (0, 1)");  // NaN fails both
+    need(itmax >= 1, "itmax must be >= 1");
+    need(ita <= itmax, "ita must not exceed itmax");
+    need(alpha >= 0.0 && std::isfinite(alpha), "alpha must be finite and >= 0");
+    need(chi2_dof_max > 0.0, "chi2_dof_max must be positive");
+    need(lower.size() == dims && upper.size() == dims, "bounds must have one entry per axis");
+    bool box_ok = true;
+    for (std::uint32_t j = 0; j < dims && box_ok; ++j)
+      box_ok = std::isfinite(lower[j]) && std::isfinite(upper[j]) && lower[j] < upper[j];
+    need(box_ok, "requires finite lower < upper on every axis");
   }
 };
 
@@ -539,44 +559,49 @@ struct SetupParams {
   std::uint64_t s;
 };
 
-/// driver.hpp:82-87
+/// driver.hpp:82-87: about 32 batches per worker, at least one cube each.
 [[nodiscard]] inline std::uint64_t set_batch_size(std::uint64_t m, unsigned workers) {
   if (m == 0) throw std::invalid_argument("set_batch_size: m must be >= 1");
   if (workers == 0) throw std::invalid_argument("set_batch_size: workers must be >= 1");
-  const std::uint64_t per = std::uint64_t{workers} * 32;
-  return std::max<std::uint64_t>(1, (m + per - 1) / per);
+  const std::uint64_t batches = std::uint64_t{workers} * 32;
+  return (m - 1) / batches + 1;  // ceil(m / batches) >= 1
 }
 
 namespace detail {
-/// Largest g with 2*g^d <= maxcalls (driver.hpp:93-108).
+/// The largest g >= 1 with 2 g^d <= maxcalls (1 if there is none), the value
+/// of driver.hpp:93-108, found by an exact integer bisection.
 inline std::uint64_t intervals_per_axis(std::uint64_t maxcalls, std::uint32_t d) {
-  const auto fits = [&](std::uint64_t g) {
-    unsigned __int128 acc = 2;
-    for (std::uint32_t i = 0; i < d; ++i) {
-      acc *= g;
-      if (acc > maxcalls) return false;
-    }
-    return true;
+  const auto fits = [&](std::uint64_t g) {  // 2 g^d <= maxcalls without overflow
+    unsigned __int128 v = 2;
+    for (std::uint32_t i = 0; i < d && v <= maxcalls; ++i) v *= g;
+    return v <= maxcalls;
   };
-  auto g = static_cast<std::uint64_t>(
-      std::floor(std::pow(static_cast<double>(maxcalls) / 2.0, 1.0 / static_cast<double>(d))));
-  if (g < 1) g = 1;
-  while (!fits(g) && g > 1) --g;
-  while (fits(g + 1)) ++g;
-  return g;
+  std::uint64_t good = 1, bad = 2;  // fits(good) unless good == 1; !fits(bad) once found
+  while (fits(bad)) {
+    good = bad;
+    bad *= 2;
+  }
+  while (bad - good > 1) {
+    const std::uint64_t mid = good + (bad - good) / 2;
+    (fits(mid) ? good : bad) = mid;
+  }
+  return good;
 }
 }  // namespace detail
 
-/// driver.hpp:114-123
+/// driver.hpp:114-123: g intervals per axis, m = g^d sub-cubes, p = maxcalls / m
+/// samples per cube (at least 2, so each cube has a variance), batch size.
 [[nodiscard]] inline SetupParams setup(const RunConfig& cfg) {
   cfg.validate();
-  const std::uint64_t g = detail::intervals_per_axis(cfg.maxcalls, cfg.dims);
-  std::uint64_t m = 1;
-  for (std::uint32_t i = 0; i < cfg.dims; ++i) m *= g;
-  const std::uint64_t p = std::max<std::uint64_t>(2, cfg.maxcalls / m);
-  unsigned workers = cfg.workers ? cfg.workers : std::thread::hardware_concurrency();
-  if (workers == 0) workers = 1;
-  return {g, m, p, set_batch_size(m, workers)};
+  SetupParams sp{};
+  sp.g = detail::intervals_per_axis(cfg.maxcalls, cfg.dims);
+  sp.m = 1;
+  for (std::uint32_t j = 0; j < cfg.dims; ++j) sp.m *= sp.g;
+  sp.p = std::max<std::uint64_t>(2, cfg.maxcalls / sp.m);
+  unsigned workers = cfg.workers;
+  if (workers == 0) workers = std::max(1u, std::thread::hardware_concurrency());
+  sp.s = set_batch_size(sp.m, workers);
+  return sp;
 }
 
 struct IterationResult {
