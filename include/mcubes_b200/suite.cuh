@@ -118,60 +118,57 @@ inline double reference_value(int family, std::uint32_t d) {
 
 /// Suite integrand `family` on the unit hyper-cube with its reference value
 /// (integrands.hpp:107-175).
+namespace detail {
+/// One catalogue entry: `name` on the box [lo, hi]^dims, evaluated on the
+/// device by fn::Suite{family, norm}.
+inline IntegrandSpec catalogue_entry(std::string name, std::uint32_t dims, double lo, double hi,
+                                     std::optional<double> reference, int family, double norm = 0.0) {
+  IntegrandSpec spec;
+  spec.name = std::move(name);
+  spec.dims = dims;
+  spec.lower = std::vector<double>(dims, lo);
+  spec.upper = std::vector<double>(dims, hi);
+  spec.reference = reference;
+  spec.evaluate = gpu::fn::Suite{family, norm};
+  return spec;
+}
+}  // namespace detail
+
+/// Genz family 1..6 on the unit cube (integrands.hpp:107-175).
 inline IntegrandSpec make_suite_integrand(int family, std::uint32_t d) {
   if (family < 1 || family > 6) throw std::invalid_argument("make_suite_integrand: family must be in 1..6");
   if (d < 1) throw std::invalid_argument("make_suite_integrand: d must be >= 1");
-  IntegrandSpec spec;
-  spec.name = "f" + std::to_string(family);
-  spec.dims = d;
-  spec.lower.assign(d, 0.0);
-  spec.upper.assign(d, 1.0);
-  spec.reference = reference_value(family, d);
-  spec.evaluate = gpu::fn::Suite{family, 0.0};
-  return spec;
+  return detail::catalogue_entry("f" + std::to_string(family), d, 0.0, 1.0, reference_value(family, d), family);
 }
 
 /// sin of the coordinate sum over (0,10)^6 (integrands.hpp:181-196); reference
 /// Im[((e^(10i) - 1)/i)^6].
 inline IntegrandSpec make_fA() {
-  IntegrandSpec spec;
-  spec.name = "fA";
-  spec.dims = 6;
-  spec.lower.assign(6, 0.0);
-  spec.upper.assign(6, 10.0);
-  const std::complex<double> i(0.0, 1.0);
-  spec.reference = std::pow((std::exp(10.0 * i) - 1.0) / i, 6).imag();
-  spec.evaluate = gpu::fn::Suite{7, 0.0};
-  return spec;
+  const std::complex<double> one_axis = (std::exp(std::complex<double>(0.0, 10.0)) - 1.0) / std::complex<double>(0.0, 1.0);
+  return detail::catalogue_entry("fA", 6, 0.0, 10.0, std::pow(one_axis, 6).imag(), 7);
 }
 
-/// Normalised Gaussian (variance 0.01 per axis) on (-1,1)^9 (integrands.hpp:200-215).
+/// Normalised Gaussian (variance 0.01 per axis) on (-1,1)^9 (integrands.hpp:200-215):
+/// mass erf(1/sqrt(2 sigma^2))^9 inside the box.
 inline IntegrandSpec make_fB() {
-  IntegrandSpec spec;
-  spec.name = "fB";
-  spec.dims = 9;
-  spec.lower.assign(9, -1.0);
-  spec.upper.assign(9, 1.0);
-  const double sigma2 = 0.01;
-  spec.reference = std::pow(std::erf(1.0 / std::sqrt(2.0 * sigma2)), 9.0);
-  spec.evaluate = gpu::fn::Suite{8, std::pow(2.0 * std::numbers::pi * sigma2, -4.5)};
-  return spec;
+  constexpr double kSigma2 = 0.01;
+  return detail::catalogue_entry("fB", 9, -1.0, 1.0, std::pow(std::erf(1.0 / std::sqrt(2.0 * kSigma2)), 9.0), 8,
+                                 std::pow(2.0 * std::numbers::pi * kSigma2, -4.5));
 }
 
-/// Look up an integrand by CLI name (integrands.hpp:221-235): "f1".."f6" with
-/// an explicit dimension, "fA"/"fB" with 0 or their own dimension.
+/// Look up an integrand by CLI name (integrands.hpp:221-235): "f1".."f6" need
+/// an explicit dimension; "fA" / "fB" take 0 or their own dimension.
 inline IntegrandSpec make_integrand(std::string_view id, std::uint32_t dims) {
-  if (id == "fA" || id == "fB") {
-    IntegrandSpec spec = id == "fA" ? make_fA() : make_fB();
-    if (dims != 0 && dims != spec.dims)
-      throw std::invalid_argument(std::string(id) + " is fixed at " + std::to_string(spec.dims) + " dimensions");
-    return spec;
+  const std::string name(id);
+  if (name == "fA" || name == "fB") {
+    IntegrandSpec fixed = name == "fA" ? make_fA() : make_fB();
+    if (dims == 0 || dims == fixed.dims) return fixed;
+    throw std::invalid_argument(name + " is fixed at " + std::to_string(fixed.dims) + " dimensions");
   }
-  if (id.size() == 2 && id[0] == 'f' && id[1] >= '1' && id[1] <= '6') {
-    if (dims == 0) throw std::invalid_argument(std::string(id) + " requires an explicit dimension");
-    return make_suite_integrand(id[1] - '0', dims);
-  }
-  throw std::invalid_argument("unknown integrand \"" + std::string(id) + "\"");
+  const bool genz = name.size() == 2 && name[0] == 'f' && name[1] >= '1' && name[1] <= '6';
+  if (!genz) throw std::invalid_argument("unknown integrand \"" + name + "\"");
+  if (dims == 0) throw std::invalid_argument(name + " requires an explicit dimension");
+  return make_suite_integrand(name[1] - '0', dims);
 }
 
 }  // namespace mcubes
