@@ -52,26 +52,24 @@ namespace mcubes {
 /// Per-axis, per-bin totals of (f(x)*J)^2 (accumulators.hpp:18-56).
 class BinAccumulator {
  public:
-  BinAccumulator(std::uint32_t dims, std::uint32_t n_bins)
-      : dims_(dims), n_bins_(n_bins), values_(std::size_t{dims} * n_bins, 0.0) {
-    if (dims == 0) throw std::invalid_argument("BinAccumulator: dims must be >= 1");
-    if (n_bins == 0) throw std::invalid_argument("BinAccumulator: n_bins must be >= 1");
+  BinAccumulator(std::uint32_t dims, std::uint32_t n_bins) : dims_(dims), n_bins_(n_bins) {
+    if (dims == 0) invalid("dims must be >= 1");
+    if (n_bins == 0) invalid("n_bins must be >= 1");
+    values_.assign(cells(), 0.0);
   }
+  /// The GPU's result: device-rounded cell values and the device-counted writes.
   BinAccumulator(std::uint32_t dims, std::uint32_t n_bins, std::vector<double> values, std::uint64_t writes)
       : dims_(dims), n_bins_(n_bins), values_(std::move(values)), writes_(writes) {
-    if (values_.size() != std::size_t{dims} * n_bins)
-      throw std::invalid_argument("BinAccumulator: value matrix has wrong shape");
+    if (values_.size() != cells()) invalid("value matrix has wrong shape");
   }
   void deposit(std::uint32_t axis, std::uint32_t bin, double v) {
-    values_[std::size_t{axis} * n_bins_ + bin] += v;
-    ++writes_;
+    values_[cell(axis, bin)] += v;
+    writes_ += 1;
   }
-  [[nodiscard]] double at(std::uint32_t axis, std::uint32_t bin) const {
-    return values_[std::size_t{axis} * n_bins_ + bin];
-  }
+  [[nodiscard]] double at(std::uint32_t axis, std::uint32_t bin) const { return values_[cell(axis, bin)]; }
   [[nodiscard]] std::span<const double> axis_row(std::uint32_t axis) const {
-    if (axis >= dims_) throw std::invalid_argument("BinAccumulator: axis out of range");
-    return {values_.data() + std::size_t{axis} * n_bins_, n_bins_};
+    if (axis >= dims_) invalid("axis out of range");
+    return std::span<const double>(values_).subspan(cell(axis, 0), n_bins_);
   }
   [[nodiscard]] const std::vector<double>& values() const { return values_; }
   [[nodiscard]] std::uint32_t dims() const { return dims_; }
@@ -79,6 +77,13 @@ class BinAccumulator {
   [[nodiscard]] std::uint64_t writes() const { return writes_; }
 
  private:
+  [[noreturn]] static void invalid(const char* what) {
+    throw std::invalid_argument(std::string("BinAccumulator: ") + what);
+  }
+  [[nodiscard]] std::size_t cells() const { return std::size_t{dims_} * n_bins_; }
+  [[nodiscard]] std::size_t cell(std::uint32_t axis, std::uint32_t bin) const {
+    return std::size_t{axis} * n_bins_ + bin;  // axis-major, as grid.hpp:303 and sampler.hpp:107-124
+  }
   std::uint32_t dims_;
   std::uint32_t n_bins_;
   std::vector<double> values_;
@@ -96,12 +101,16 @@ class NonFiniteSample : public std::runtime_error {
   [[nodiscard]] double value() const { return value_; }
 
  private:
-  static std::string describe(const std::vector<double>& x, double fx) {
-    std::ostringstream os;
-    os << "integrand produced non-finite value " << fx << " at x = (";
-    for (std::size_t j = 0; j < x.size(); ++j) os << (j ? ", " : "") << x[j];
-    os << ")";
-    return os.str();
+  static std::string describe(const std::vector<double>& x, double fx) {  // sampler.hpp:31-48's message
+    std::ostringstream msg;
+    msg << "integrand produced non-finite value " << fx << " at x = (";
+    const char* sep = "";
+    for (const double xj : x) {
+      msg << sep << xj;
+      sep = ", ";
+    }
+    msg << ')';
+    return msg.str();
   }
   std::vector<double> point_;
   double value_;
@@ -411,16 +420,16 @@ class Grid {
 /// Unit-space position of a point in cube t (sampler.hpp:75-87).
 inline void cube_unit_point(std::uint64_t t, std::uint64_t g, std::uint32_t dims, std::span<const double> r,
                             std::span<double> u) {
-  if (g == 0) throw std::invalid_argument("cube_unit_point: g must be >= 1");
-  if (r.size() != dims || u.size() != dims)
-    throw std::invalid_argument("cube_unit_point: r and u must have one entry per axis");
-  std::uint64_t tt = t;
-  const double gd = static_cast<double>(g);
-  for (std::uint32_t j = 0; j < dims; ++j) {
-    u[j] = (static_cast<double>(tt % g) + r[j]) / gd;
-    tt /= g;
+  const auto fail = [](const char* what) { throw std::invalid_argument(std::string("cube_unit_point: ") + what); };
+  if (g == 0) fail("g must be >= 1");
+  if (r.size() != dims || u.size() != dims) fail("r and u must have one entry per axis");
+  // t in base g, axis 0 the fastest digit: u_j = (digit_j + r_j) / g
+  std::uint64_t rest = t;
+  for (std::uint32_t j = 0; j < dims; ++j, rest /= g) {
+    const std::uint64_t digit = rest % g;
+    u[j] = (static_cast<double>(digit) + r[j]) / static_cast<double>(g);
   }
-  if (tt != 0) throw std::invalid_argument("cube_unit_point: cube index out of range");
+  if (rest != 0) fail("cube index out of range");
 }
 
 namespace gpu {
